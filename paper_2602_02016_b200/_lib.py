@@ -1,0 +1,87 @@
+"""ctypes binding of ``libdash_b200.so`` (the C ABI declared in ``include/dash_b200.h``).
+
+The library is the only compute path: there is no CPU or PyTorch fallback.  Loading fails loudly
+when the shared object is missing (run ``__graft_entry__.build()``), and every wrapper raises when a
+call returns a non-zero status.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+import torch
+
+from .errors import NumericalError
+
+_LIB_PATH = Path(__file__).resolve().parent / "libdash_b200.so"
+_lib: ctypes.CDLL | None = None
+
+DASH_OK, DASH_EINVAL, DASH_ENONFINITE, DASH_ECUDA = 0, 1, 2, 3
+
+c_int, c_float, c_longlong, c_size_t, c_void_p = (
+    ctypes.c_int, ctypes.c_float, ctypes.c_longlong, ctypes.c_size_t, ctypes.c_void_p)
+
+
+class dash_stack(ctypes.Structure):
+    _fields_ = [
+        ("data", c_void_p),
+        ("nmat", c_int), ("rows", c_int), ("cols", c_int), ("ld", c_int),
+        ("exp", c_void_p),
+        ("amax", c_void_p),
+    ]
+
+
+_P = ctypes.POINTER(dash_stack)
+
+# name -> (restype, argtypes); mirrors include/dash_b200.h
+_SIGNATURES: dict[str, tuple] = {
+    "dash_version": (ctypes.c_char_p, []),
+    "dash_device_sms": (c_int, []),
+    "dash_split": (c_int, [c_void_p, c_longlong, c_int, _P, c_void_p]),
+    "dash_unsplit": (c_int, [_P, c_void_p, c_longlong, c_int, c_void_p]),
+    "dash_bmm_ws_bytes": (c_size_t, [c_int]),
+    "dash_bmm": (c_int, [_P, c_int, _P, c_int, _P, c_void_p, c_longlong, c_int, c_float, c_int, c_void_p,
+                         c_size_t, c_void_p]),
+}
+
+
+def lib() -> ctypes.CDLL:
+    """Load (once) and return the C-ABI library; raises if it was not built."""
+    global _lib
+    if _lib is None:
+        if not _LIB_PATH.exists():
+            raise RuntimeError(
+                f"{_LIB_PATH} not found: the DASH CUDA extension is not built "
+                "(run `python -c 'import __graft_entry__ as g; g.build()'`). There is no CPU fallback.")
+        handle = ctypes.CDLL(str(_LIB_PATH), mode=os.RTLD_LOCAL)
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def exported_symbols() -> list[str]:
+    return list(_SIGNATURES)
+
+
+def check(status: int, what: str) -> None:
+    if status == DASH_OK:
+        return
+    if status == DASH_ENONFINITE:
+        raise NumericalError(f"{what}: non-finite values")
+    if status == DASH_EINVAL:
+        raise ValueError(f"{what}: invalid argument")
+    raise RuntimeError(f"{what}: CUDA error (status {status}): {torch.cuda.current_stream()}")
+
+
+def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def require_cuda(t: torch.Tensor, what: str) -> None:
+    if not t.is_cuda:
+        raise ValueError(f"{what} must be a CUDA tensor (the DASH B200 path has no CPU fallback)")

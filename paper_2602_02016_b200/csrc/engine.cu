@@ -1,0 +1,266 @@
+// Host runtime of the DASH engine: TMA descriptor creation, split/unsplit kernels, grouped GEMM
+// job assembly, and the dense-primitive part of the C ABI (include/dash_b200.h).
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstring>
+#include <vector>
+
+#include "engine.h"
+#include "ptx.cuh"
+
+namespace dash {
+
+// ---------------------------------------------------------------------------- TMA descriptors
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool make_stack_map(const dash_stack& s, int box_rows, CUtensorMap* out) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(s.ld), static_cast<cuuint64_t>(s.rows), 2,
+                        static_cast<cuuint64_t>(s.nmat)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(s.ld) * 2, static_cast<cuuint64_t>(s.rows) * s.ld * 2,
+                           2ull * s.rows * s.ld * 2};
+  cuuint32_t box[4] = {static_cast<cuuint32_t>(kTileK), static_cast<cuuint32_t>(box_rows), 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, s.data, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool stack_ok(const dash_stack* s) {
+  return s && s->data && s->nmat > 0 && s->rows > 0 && s->cols > 0 && s->ld >= s->cols && s->ld % kLdAlign == 0 &&
+         s->exp && s->amax;
+}
+
+// ---------------------------------------------------------------------------- split / unsplit
+__global__ void amax_kernel(const float* __restrict__ src, long long mat_stride, int ld, int rows, int cols,
+                            unsigned* __restrict__ amax) {
+  const int m = blockIdx.y;
+  const float* base = src + m * mat_stride;
+  const long long total = static_cast<long long>(rows) * cols;
+  float mx = 0.f;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(i / cols), c = static_cast<int>(i % cols);
+    float v = fabsf(base[static_cast<long long>(r) * ld + c]);
+    if (!(v <= 3.0e38f)) v = __uint_as_float(0x7fc00000u);
+    mx = nonneg_max(mx, v);
+  }
+  mx = warp_max_nonneg(mx);
+  if ((threadIdx.x & 31) == 0) atomic_max_nonneg(amax + m, mx);
+}
+
+__device__ __forceinline__ int exp_for_max(float amax) {
+  if (!(amax > 0.f) || !(amax < 3.0e38f)) return 0;
+  int x;
+  frexpf(amax, &x);
+  return x - 15;
+}
+
+__global__ void split_kernel(const float* __restrict__ src, long long mat_stride, int src_ld, int rows, int cols,
+                             __half* __restrict__ dst, int ld, const unsigned* __restrict__ amax,
+                             int* __restrict__ exp_out) {
+  const int m = blockIdx.y;
+  const int e = exp_for_max(__uint_as_float(amax[m]));
+  if (blockIdx.x == 0 && threadIdx.x == 0) exp_out[m] = e;
+  const float inv = ldexpf(1.f, -e);
+  const float* s = src + m * mat_stride;
+  __half* hi = dst + static_cast<long long>(m) * 2 * rows * ld;
+  __half* lo = hi + static_cast<long long>(rows) * ld;
+  const long long total = static_cast<long long>(rows) * ld;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(i / ld), c = static_cast<int>(i % ld);
+    float y = 0.f;
+    if (c < cols) y = s[static_cast<long long>(r) * src_ld + c] * inv;
+    const __half h = __float2half_rn(y);
+    hi[i] = h;
+    lo[i] = __float2half_rn(y - __half2float(h));
+  }
+}
+
+__global__ void unsplit_kernel(const __half* __restrict__ src, int rows, int cols, int ld,
+                               const int* __restrict__ exps, float* __restrict__ dst, long long mat_stride,
+                               int dst_ld) {
+  const int m = blockIdx.y;
+  const float sc = ldexpf(1.f, exps[m]);
+  const __half* hi = src + static_cast<long long>(m) * 2 * rows * ld;
+  const __half* lo = hi + static_cast<long long>(rows) * ld;
+  float* d = dst + m * mat_stride;
+  const long long total = static_cast<long long>(rows) * cols;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(i / cols), c = static_cast<int>(i % cols);
+    const long long o = static_cast<long long>(r) * ld + c;
+    d[static_cast<long long>(r) * dst_ld + c] = (__half2float(hi[o]) + __half2float(lo[o])) * sc;
+  }
+}
+
+static dim3 grid_for(long long elems, int nmat) {
+  long long b = (elems + 255) / 256;
+  if (b > 1024) b = 1024;
+  if (b < 1) b = 1;
+  return dim3(static_cast<unsigned>(b), static_cast<unsigned>(nmat));
+}
+
+int split_stack(const float* src, long long mat_stride, int src_ld, const dash_stack& d, cudaStream_t st) {
+  cudaMemsetAsync(d.amax, 0, sizeof(unsigned) * d.nmat, st);
+  amax_kernel<<<grid_for(static_cast<long long>(d.rows) * d.cols, d.nmat), 256, 0, st>>>(
+      src, mat_stride, src_ld, d.rows, d.cols, d.amax);
+  split_kernel<<<grid_for(static_cast<long long>(d.rows) * d.ld, d.nmat), 256, 0, st>>>(
+      src, mat_stride, src_ld, d.rows, d.cols, reinterpret_cast<__half*>(d.data), d.ld, d.amax, d.exp);
+  return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ECUDA;
+}
+
+int unsplit_stack(const dash_stack& s, float* dst, long long mat_stride, int dst_ld, cudaStream_t st) {
+  unsplit_kernel<<<grid_for(static_cast<long long>(s.rows) * s.cols, s.nmat), 256, 0, st>>>(
+      reinterpret_cast<const __half*>(s.data), s.rows, s.cols, s.ld, s.exp, dst, mat_stride, dst_ld);
+  return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ECUDA;
+}
+
+// ---------------------------------------------------------------------------- job assembly
+int JobBuilder::add_map(const dash_stack& s, int box_rows) {
+  for (size_t i = 0; i < map_keys.size(); ++i)
+    if (map_keys[i].data == s.data && map_keys[i].box == box_rows && map_keys[i].nmat == s.nmat &&
+        map_keys[i].rows == s.rows && map_keys[i].ld == s.ld)
+      return static_cast<int>(i);
+  CUtensorMap m;
+  if (!make_stack_map(s, box_rows, &m)) return -1;
+  maps.push_back(m);
+  map_keys.push_back(MapKey{s.data, box_rows, s.nmat, s.rows, s.ld});
+  return static_cast<int>(maps.size()) - 1;
+}
+
+// Fill operand fields of `j` for C = op(A) op(B); returns false on a shape mismatch or map failure.
+bool JobBuilder::operands(GemmJob& j, const dash_stack& a, int am, int trans_a, const dash_stack& b, int bm,
+                          int trans_b) {
+  const int M = trans_a ? a.cols : a.rows;
+  const int K = trans_a ? a.rows : a.cols;
+  const int Kb = trans_b ? b.cols : b.rows;
+  const int N = trans_b ? b.rows : b.cols;
+  if (K != Kb) return false;
+  std::memset(&j, 0, sizeof(j));
+  j.a_mn = trans_a ? 1 : 0;  // stored K x M -> MN-major
+  j.b_mn = trans_b ? 0 : 1;  // stored K x N -> MN-major; stored N x K -> K-major
+  j.a_map = add_map(a, j.a_mn ? 64 : kTileM);
+  j.b_map = add_map(b, j.b_mn ? 64 : kTileN);
+  if (j.a_map < 0 || j.b_map < 0) return false;
+  j.a_mat = am;
+  j.b_mat = bm;
+  j.M = M;
+  j.N = N;
+  j.K = K;
+  j.tiles_n = (N + kTileN - 1) / kTileN;
+  j.a_exp = a.exp + am;
+  j.a_amax = a.amax + am;
+  j.b_exp = b.exp + bm;
+  j.b_amax = b.amax + bm;
+  j.alpha = 1.f;
+  return true;
+}
+
+void JobBuilder::set_out(GemmJob& j, const dash_stack& c, int cm) {
+  j.c_hi = reinterpret_cast<__half*>(c.data) + static_cast<long long>(cm) * 2 * c.rows * c.ld;
+  j.c_plane = static_cast<long long>(c.rows) * c.ld;
+  j.c_ld = c.ld;
+  j.c_exp = c.exp + cm;
+  j.c_amax = c.amax + cm;
+}
+
+void JobBuilder::push(GemmJob& j) {
+  j.tile_start = tiles;
+  tiles += ((j.M + kTileM - 1) / kTileM) * j.tiles_n;
+  jobs.push_back(j);
+}
+
+size_t JobBuilder::bytes_for(int nmaps, int njobs) {
+  return static_cast<size_t>(nmaps) * sizeof(CUtensorMap) + static_cast<size_t>(njobs) * sizeof(GemmJob) + 256;
+}
+
+int JobBuilder::launch(void* ws, size_t ws_bytes, int passes, cudaStream_t st) {
+  if (jobs.empty()) return DASH_OK;
+  const size_t need = bytes_for(static_cast<int>(maps.size()), static_cast<int>(jobs.size()));
+  if (!ws || ws_bytes < need) return DASH_EINVAL;
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ws) + 127) & ~uintptr_t(127));
+  CUtensorMap* d_maps = reinterpret_cast<CUtensorMap*>(base);
+  GemmJob* d_jobs = reinterpret_cast<GemmJob*>(base + maps.size() * sizeof(CUtensorMap));
+  // one host staging block -> one H2D copy
+  staging.resize(maps.size() * sizeof(CUtensorMap) + jobs.size() * sizeof(GemmJob));
+  std::memcpy(staging.data(), maps.data(), maps.size() * sizeof(CUtensorMap));
+  std::memcpy(staging.data() + maps.size() * sizeof(CUtensorMap), jobs.data(), jobs.size() * sizeof(GemmJob));
+  if (cudaMemcpyAsync(base, staging.data(), staging.size(), cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return DASH_ECUDA;
+  return gemm_launch(d_jobs, static_cast<int>(jobs.size()), tiles, d_maps, passes, st);
+}
+
+}  // namespace dash
+
+// ============================================================================ C ABI
+using namespace dash;
+
+extern "C" {
+
+const char* dash_version(void) { return "dash-b200 0.1 (sm_100a tcgen05)"; }
+
+int dash_device_sms(void) {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+int dash_split(const float* src, long long src_mat_stride, int src_ld, const dash_stack* dst, void* stream) {
+  if (!src || !stack_ok(dst) || src_ld < dst->cols) return DASH_EINVAL;
+  return split_stack(src, src_mat_stride, src_ld, *dst, static_cast<cudaStream_t>(stream));
+}
+
+int dash_unsplit(const dash_stack* src, float* dst, long long dst_mat_stride, int dst_ld, void* stream) {
+  if (!stack_ok(src) || !dst || dst_ld < src->cols) return DASH_EINVAL;
+  return unsplit_stack(*src, dst, dst_mat_stride, dst_ld, static_cast<cudaStream_t>(stream));
+}
+
+size_t dash_bmm_ws_bytes(int nmat) { return JobBuilder::bytes_for(8, nmat); }
+
+int dash_bmm(const dash_stack* a, int trans_a, const dash_stack* b, int trans_b, const dash_stack* c,
+             float* f_out, long long f_mat_stride, int f_ld, float alpha, int passes, void* ws, size_t ws_bytes,
+             void* stream) {
+  if (!stack_ok(a) || !stack_ok(b) || (c && !stack_ok(c)) || (!c && !f_out)) return DASH_EINVAL;
+  if (a->nmat != b->nmat || (c && c->nmat != a->nmat) || (passes != 1 && passes != 3)) return DASH_EINVAL;
+  const int M = trans_a ? a->cols : a->rows;
+  const int N = trans_b ? b->rows : b->cols;
+  if (c && (c->rows != M || c->cols != N)) return DASH_EINVAL;
+  if (f_out && f_ld < N) return DASH_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  JobBuilder jb;
+  if (c) cudaMemsetAsync(c->amax, 0, sizeof(unsigned) * c->nmat, st);
+  for (int m = 0; m < a->nmat; ++m) {
+    GemmJob j;
+    if (!jb.operands(j, *a, m, trans_a, *b, m, trans_b)) return DASH_EINVAL;
+    j.op = EPI_SPLIT;
+    j.alpha = alpha;
+    j.out_mat = m;
+    if (c) jb.set_out(j, *c, m);
+    if (f_out) {
+      j.f_out = f_out + m * f_mat_stride;
+      j.f_ld = f_ld;
+    }
+    jb.push(j);
+  }
+  return jb.launch(ws, ws_bytes, passes, st);
+}
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+// Shared host/device data structures of the DASH B200 engine.
+//
+// Matrix storage ("split-f16 stack"): a stack of `nmat` matrices of `rows x cols`, each stored as two
+// fp16 planes (hi, lo) of `rows x ld` (ld = cols rounded up to 64, zero padded) plus a per-matrix
+// power-of-two exponent e and a running max-abs `amax`:
+//     value[m][r][c] = (hi[m][r][c] + lo[m][r][c]) * 2^e[m]
+// hi = RN16(x * 2^-e), lo = RN16(x * 2^-e - hi).  e is chosen so |x| * 2^-e < 2^15, which keeps both
+// planes in the fp16 normal range for every entry within 2^-18 of the matrix max (22-bit significand,
+// i.e. fp32-class accuracy) -- see DESIGN.md "split-f16 format".
+#pragma once
+#include <cstdint>
+
+#ifdef __CUDACC__
+#include <cuda_fp16.h>
+#define DASH_HD __host__ __device__
+#else
+#define DASH_HD
+struct __half { unsigned short x; };
+#endif
+
+namespace dash {
+
+constexpr int kTileM = 128;   // UMMA M (one CTA)
+constexpr int kTileN = 256;   // UMMA N
+constexpr int kTileK = 64;    // fp16 elements per 128-byte swizzle row
+constexpr int kLdAlign = 64;  // leading-dimension padding of split stacks (elements)
+constexpr int kEExp = -13;    // fixed exponent of identity-like Newton factors E (|E| < 8)
+
+enum EpiOp : int {
+  EPI_SPLIT = 0,       // C = alpha * alpha_p[mat] * acc                 -> split (+ optional fp32)
+  EPI_NDB_E = 1,       // E = 1.5 I - 0.5 acc (E = I when inactive)     -> split, residual max|E-I|
+  EPI_EMA = 2,         // F = beta * F_in + (1 - beta) * acc            -> fp32 only
+  EPI_CHEB = 3,        // B = 2 acc - S + c I                           -> split
+  EPI_CHEB_FINAL = 4,  // R = (acc - S + c I) * alpha_p[mat]            -> fp32 + split
+  EPI_APPLY = 5,       // U = acc                                       -> fp32, per-tile sum(U^2)
+  EPI_CN_M = 6,        // M = acc -> split, residual max|M-I|, and corr C = (1+1/p) I - M/p -> split #2
+};
+
+// One output matrix of a grouped GEMM: C[M x N] = op(A)[M x K] * op(B)[K x N], then epilogue.
+// Operand majorness (tcgen05 terms): A K-major = stored row-major M x K; A MN-major = stored K x M.
+//                                    B K-major = stored N x K;           B MN-major = stored K x N.
+struct GemmJob {
+  // ---- operands (TMA maps index into the map table; mat = coordinate along the stack)
+  int a_map, b_map;
+  int a_mat, b_mat;
+  int a_mn, b_mn;
+  int M, N, K;
+  int tiles_n;  // ceil(N / kTileN)
+  int tile_start;  // first global tile index of this job
+  int op;
+  int out_mat;     // index into per-matrix epilogue arrays (resid, active, alpha_p)
+  int c_ld;        // split output leading dim
+  int f_ld;        // fp32 output / input leading dim
+  int s_ld;        // side split input leading dim
+  int pad0;
+  const int* a_exp;  const unsigned* a_amax;   // exponent / amax of the A matrix
+  const int* b_exp;  const unsigned* b_amax;
+  // ---- split output (hi plane; lo plane at +c_plane elements)
+  __half* c_hi; long long c_plane; int* c_exp; unsigned* c_amax;
+  // ---- second split output (EPI_CN_M correction factor)
+  __half* c2_hi; long long c2_plane; int* c2_exp; unsigned* c2_amax;
+  // ---- fp32 output / input
+  float* f_out; const float* f_in;
+  // ---- side split input (EPI_CHEB*: B_{k+2})
+  const __half* s_hi; long long s_plane; const int* s_exp; const unsigned* s_amax;
+  // ---- scalars
+  float alpha; float beta; float gamma; float pad1;
+  const float* alpha_p;   // per-matrix multiplier (indexed by out_mat) or null
+  unsigned* resid;        // per-matrix residual accumulator (indexed by out_mat) or null
+  const int* active;      // per-matrix active flag (indexed by out_mat) or null
+  float* partial;         // EPI_APPLY: per-(tile, quarter) partial sums, indexed by local tile
+};
+
+}  // namespace dash

@@ -1,0 +1,210 @@
+"""Dense primitives on the B200: precision modes, split-f16 stacks, the batched product.
+
+Mirrors the reference's ``linalg.py`` surface (``PrecisionMode`` ``:23-25``, ``matrix``/``batched``
+``:28-47``, ``count_matmuls`` ``:50-72``, ``bmm`` ``:105-114``, ``symmetrize`` ``:121-124``) but every
+product runs through the C-ABI tcgen05 engine (``csrc/gemm_tc.cu``).
+
+Precision modes (the reference has FULL64 / EMULATED32; the B200 build adds F16):
+
+* ``EMULATED32`` ("f32") -- split-f16 products: each operand is stored as fp16 hi + fp16 lo with a
+  per-matrix power-of-two exponent, and every product issues hi*hi + hi*lo + lo*hi on the tensor
+  cores with fp32 accumulation (22-bit significands, fp32-class results).
+* ``FULL64`` ("f64") -- accepted for drop-in compatibility; runs the same split-f16 engine (there is
+  no fp64 tensor-core path on the hot path).  Parity against the float64 reference is therefore by
+  the tolerances stated in DESIGN.md, never bitwise.
+* ``F16`` ("f16") -- hi*hi only (fp16 tensor rate, ~11-bit significands).
+"""
+from __future__ import annotations
+
+import contextlib
+import ctypes
+import enum
+from typing import Iterator
+
+import numpy as np
+import torch
+
+from . import _lib
+
+LD_ALIGN = 64
+
+
+class PrecisionMode(enum.Enum):
+    FULL64 = "f64"
+    EMULATED32 = "f32"
+    F16 = "f16"
+
+
+def passes_for(mode: PrecisionMode) -> int:
+    return 1 if mode is PrecisionMode.F16 else 3
+
+
+def _ld(cols: int) -> int:
+    return (cols + LD_ALIGN - 1) // LD_ALIGN * LD_ALIGN
+
+
+def device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("the DASH B200 path needs a CUDA device (there is no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+class SplitStack:
+    """A stack of ``nmat`` ``rows x cols`` matrices in split-f16 form (see csrc/types.h).
+
+    ``data``: fp16 tensor (nmat, 2, rows, ld); ``exp``: int32 (nmat,); ``amax``: int32 (nmat,) holding
+    float bit patterns.  value = (hi + lo) * 2**exp.
+    """
+
+    __slots__ = ("data", "exp", "amax", "rows", "cols", "_c")
+
+    def __init__(self, nmat: int, rows: int, cols: int, dev: torch.device | None = None):
+        dev = dev or device()
+        self.rows, self.cols = rows, cols
+        self.data = torch.zeros((nmat, 2, rows, _ld(cols)), dtype=torch.float16, device=dev)
+        self.exp = torch.zeros(nmat, dtype=torch.int32, device=dev)
+        self.amax = torch.zeros(nmat, dtype=torch.int32, device=dev)
+        self._c = None
+
+    @property
+    def nmat(self) -> int:
+        return self.data.shape[0]
+
+    @property
+    def ld(self) -> int:
+        return self.data.shape[3]
+
+    def c(self) -> _lib.dash_stack:
+        if self._c is None:
+            self._c = _lib.dash_stack(self.data.data_ptr(), self.nmat, self.rows, self.cols, self.ld,
+                                      self.exp.data_ptr(), self.amax.data_ptr())
+        return self._c
+
+    def ref(self):
+        return ctypes.byref(self.c())
+
+    @classmethod
+    def from_float(cls, x: torch.Tensor) -> "SplitStack":
+        """Split an fp32 (nmat, rows, cols) CUDA tensor."""
+        _lib.require_cuda(x, "input")
+        x = x.to(torch.float32)
+        if x.dim() == 2:
+            x = x[None]
+        if x.stride(2) != 1:
+            x = x.contiguous()
+        s = cls(x.shape[0], x.shape[1], x.shape[2], x.device)
+        s.load(x)
+        return s
+
+    def load(self, x: torch.Tensor) -> "SplitStack":
+        if x.stride(2) != 1:
+            x = x.contiguous()
+        _lib.check(_lib.lib().dash_split(x.data_ptr(), x.stride(0), x.stride(1), self.ref(), _lib.stream_ptr()),
+                   "dash_split")
+        return self
+
+    def to_float(self) -> torch.Tensor:
+        out = torch.empty((self.nmat, self.rows, self.cols), dtype=torch.float32, device=self.data.device)
+        _lib.check(_lib.lib().dash_unsplit(self.ref(), out.data_ptr(), out.stride(0), out.stride(1),
+                                           _lib.stream_ptr()), "dash_unsplit")
+        return out
+
+    def amax_float(self) -> torch.Tensor:
+        return self.amax.view(torch.float32)
+
+
+def workspace(nbytes: int, dev: torch.device | None = None) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=dev or device())
+
+
+# ----------------------------------------------------------------------------- matmul accounting
+class MatmulCounter:
+    """Counts matmul/bmm invocations while installed via count_matmuls() (linalg.py:50-67)."""
+
+    def __init__(self) -> None:
+        self.count = 0
+
+
+_ACTIVE_COUNTERS: list[MatmulCounter] = []
+
+
+@contextlib.contextmanager
+def count_matmuls() -> Iterator[MatmulCounter]:
+    counter = MatmulCounter()
+    _ACTIVE_COUNTERS.append(counter)
+    try:
+        yield counter
+    finally:
+        _ACTIVE_COUNTERS.remove(counter)
+
+
+def tally(n: int = 1) -> None:
+    for counter in _ACTIVE_COUNTERS:
+        counter.count += n
+
+
+# ----------------------------------------------------------------------------- validation
+def as_device_f32(data, what: str = "tensor") -> torch.Tensor:
+    if isinstance(data, torch.Tensor):
+        t = data
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(data, dtype=np.float64)))
+    return t.to(device=device(), dtype=torch.float32)
+
+
+def batched(data) -> torch.Tensor:
+    """Validate and return an (N, B, B) stack of square blocks as fp32 on the GPU (linalg.py:38-47)."""
+    a = as_device_f32(data)
+    if a.dim() != 3:
+        raise ValueError(f"batched tensor must be 3-D, got shape {tuple(a.shape)}")
+    if a.shape[1] != a.shape[2]:
+        raise ValueError(f"blocks must be square, got shape {tuple(a.shape)}")
+    if not bool(torch.isfinite(a).all()):
+        raise ValueError("batched tensor entries must be finite")
+    return a
+
+
+def matrix(data) -> torch.Tensor:
+    a = as_device_f32(data)
+    if a.dim() != 2:
+        raise ValueError(f"matrix must be 2-D, got shape {tuple(a.shape)}")
+    if not bool(torch.isfinite(a).all()):
+        raise ValueError("matrix entries must be finite")
+    return a
+
+
+# ----------------------------------------------------------------------------- products
+def bmm_split(a: SplitStack, b: SplitStack, *, trans_a: bool = False, trans_b: bool = False,
+              out: SplitStack | None = None, f_out: torch.Tensor | None = None, alpha: float = 1.0,
+              mode: PrecisionMode = PrecisionMode.EMULATED32) -> None:
+    """C[m] = alpha * op(A[m]) @ op(B[m]) on the tcgen05 engine, into a split stack and/or fp32."""
+    L = _lib.lib()
+    ws = workspace(L.dash_bmm_ws_bytes(a.nmat), a.data.device)
+    fp, fs, fl = (0, 0, 0) if f_out is None else (f_out.data_ptr(), f_out.stride(0), f_out.stride(1))
+    st = L.dash_bmm(a.ref(), int(trans_a), b.ref(), int(trans_b), out.ref() if out is not None else None,
+                    fp, fs, fl, float(alpha), passes_for(mode), ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+    _lib.check(st, "dash_bmm")
+    tally()
+
+
+def bmm(a, b, mode: PrecisionMode = PrecisionMode.EMULATED32, *, trans_a: bool = False,
+        trans_b: bool = False) -> torch.Tensor:
+    """Blockwise product on the GPU (reference ``bmm``, linalg.py:105-114): block i = a[i] @ b[i]."""
+    a = as_device_f32(a)
+    b = as_device_f32(b)
+    if a.dim() != 3 or b.dim() != 3:
+        raise ValueError("bmm expects 3-D operands")
+    sa, sb = SplitStack.from_float(a), SplitStack.from_float(b)
+    m = a.shape[2] if trans_a else a.shape[1]
+    n = b.shape[1] if trans_b else b.shape[2]
+    k_a = a.shape[1] if trans_a else a.shape[2]
+    k_b = b.shape[2] if trans_b else b.shape[1]
+    if a.shape[0] != b.shape[0] or k_a != k_b:
+        raise ValueError(f"shape mismatch: {tuple(a.shape)} x {tuple(b.shape)}")
+    out = torch.empty((a.shape[0], m, n), dtype=torch.float32, device=a.device)
+    bmm_split(sa, sb, trans_a=trans_a, trans_b=trans_b, f_out=out, mode=mode)
+    return out
+
+
+def symmetrize(a: torch.Tensor) -> torch.Tensor:
+    return (a + a.transpose(-1, -2)) * 0.5
