@@ -34,6 +34,19 @@ typedef struct dash_stack {
   uint32_t* amax;     /* [nmat] float bit patterns of max |value| (NaN bits = non-finite seen) */
 } dash_stack;
 
+/* One gradient block of a 2-D layer (or one chunk of a 1-D layer, as a rows x 1 matrix) in the flat
+ * parameter space, with the preconditioner slots it feeds (shampoo.py:176-230: SlotRef(group, slot)). */
+typedef struct dash_block {
+  long long off;            /* flat offset of element (r0, c0) */
+  int ld;                   /* row stride of the layer (1-D chunks: 1) */
+  int rows, cols;           /* block shape (1-D chunk: len x 1) */
+  int group_l, slot_l;      /* left preconditioner */
+  int group_r, slot_r;      /* right preconditioner (-1 for 1-D chunks) */
+} dash_block;
+
+/* Opaque per-structure plan: owns the grouped-GEMM job tables of one optimizer structure. */
+typedef struct dash_plan dash_plan;
+
 /* Library / build identification. */
 const char* dash_version(void);
 int dash_device_sms(void);
@@ -53,6 +66,71 @@ size_t dash_bmm_ws_bytes(int nmat);
 int dash_bmm(const dash_stack* a, int trans_a, const dash_stack* b, int trans_b, const dash_stack* c,
              float* f_out, long long f_mat_stride, int f_ld, float alpha, int passes, void* ws,
              size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------- inverse-root solvers (roots.py)
+ * Inputs are split stacks of square blocks a (N x B x B); the solvers run on a_hat = a * inv_scale[m]
+ * (inv_scale may be NULL = 1), i.e. the reference's a / scales (shampoo.py:326).  Per-block reports are
+ * written to device arrays iters[N], resid[N] (float), conv[N] (0/1) exactly as IterationReport
+ * (roots.py:32-36).  tol = 0 is fixed-iteration mode.  passes: 3 = split-f16 (fp32-class), 1 = fp16.
+ *
+ * dash_ndb: batched Newton-Denman-Beavers (roots.batched_newton_db, roots.py:262-305):
+ *   y <- a_hat^(1/2), z <- a_hat^(-1/2). */
+size_t dash_ndb_ws_bytes(int n, int b);
+int dash_ndb(const dash_stack* a, const float* inv_scale, const dash_stack* y, const dash_stack* z, float tol,
+             int max_iters, int passes, int* iters, float* resid, int* conv, void* ws, size_t ws_bytes,
+             void* stream);
+/* dash_cn: batched coupled Newton (roots.batched_coupled_newton, roots.py:216-259): x <- a_hat^(-1/p),
+ *   p in {2, 4}, c = CnConfig.resolved_c (roots.py:53-56). */
+size_t dash_cn_ws_bytes(int n, int b);
+int dash_cn(const dash_stack* a, const float* inv_scale, int p, float c, const dash_stack* x, float tol,
+            int max_iters, int passes, int* iters, float* resid, int* conv, void* ws, size_t ws_bytes,
+            void* stream);
+/* dash_scale_stack: v = value * mult[m]^pw -> fp32 f_out and/or split dst (the root rescale
+ *   roots * scales^(-1/p), shampoo.py:348, with mult = 1/scale and pw = 1/p). */
+int dash_scale_stack(const dash_stack* src, const float* mult, float pw, float* f_out, long long f_mat_stride,
+                     int f_ld, const dash_stack* dst, void* stream);
+/* dash_clenshaw: optimized matrix Clenshaw of a Chebyshev series (chebyshev.batched_clenshaw_matrix,
+ *   chebyshev.py:137-184) on S = 2 a inv_scale - I with coefficients coeffs[0..degree] (fit on the host,
+ *   chebyshev.py:46-84), result * mult[m] -> fp32 f_out ([m][B][B]) and/or split out.  d-1 products. */
+size_t dash_cheb_ws_bytes(int n, int b);
+int dash_clenshaw(const dash_stack* a, const float* inv_scale, const float* mult, const double* coeffs, int degree,
+                  float* f_out, const dash_stack* out, int passes, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------- optimizer step (shampoo.py)
+ * dash_plan_create: register the block table (matrix blocks first, then 1-D chunks), the groups'
+ * fp32 EMA stacks gema[g] ([gsize][gdim][gdim]) and split root stacks groot[g], and the flat buffers
+ * (grad/adam/mom over the flat parameter space; gsm/gsv split gradient stacks; tm split temp; um/uv fp32
+ * update stacks; pn_part/un_part/gamax/graft_s per-block scratch).  Builds and uploads the statistics and
+ * apply GEMM job tables into ws (size dash_plan_ws_bytes).  Returns NULL on error (status set). */
+size_t dash_plan_ws_bytes(int nb_m, int nb_v);
+dash_plan* dash_plan_create(const dash_block* blocks, int nb_m, int nb_v, int block_size, int ngroups,
+                            const int* gdim, const int* gsize, float* const* gema, const dash_stack* groot,
+                            float* grad, float* adam, float* mom, const dash_stack* gsm, const dash_stack* gsv,
+                            const dash_stack* tm, float* um, float* uv, float* pn_part, float* un_part,
+                            uint32_t* gamax, float* graft_s, float beta_lr, int passes, void* ws, size_t ws_bytes,
+                            void* stream, int* status);
+void dash_plan_destroy(dash_plan* p);
+int dash_plan_un_stride(const dash_plan* p);
+int dash_prep_parts(void);
+/* accumulate (shampoo.py:238-278): Adam / momentum EMA, block split of the gradient, L/R statistics EMA
+ * as grouped tcgen05 GEMMs, and the per-block graft-direction norms |P_b|^2 for n_acc = t + 1. */
+int dash_plan_accumulate(dash_plan* p, float beta2, float beta1, int n_acc, float graft_eps, void* stream);
+/* apply + graft (shampoo.py:380-403): U = rootL G rootR (1-D: rootL g), s_b = |P_b| / |U_b|,
+ * theta_out = theta_in - eta s_b U_b. */
+int dash_plan_apply(dash_plan* p, const float* theta_in, float* theta_out, float eta, void* stream);
+/* Per-group refresh helpers (shampoo.py:312-349): symmetrize the EMA (linalg.symmetrize) and collect
+ * max|a| / sum(a^2) partials of a = ema + eps I; split a; Frobenius scale; pooled power iteration
+ * (spectral.py:87-117, block seeds block_seed(seed, i), NumPy-identical start vectors).
+ * status[i]: 0 ok, 1 non-positive scale, 2 pool collapsed twice. */
+int dash_group_sym(float* ema, int n, int d, float eps, uint32_t* amax, float* fro_part, void* stream);
+int dash_group_split_a(const float* ema, float eps, const dash_stack* a, void* stream);
+int dash_fro_scale(const float* fro_part, int n, float* scale, float* inv_scale, void* stream);
+int dash_power_iteration(const float* ema, int n, int d, float eps, int pool, int iters, unsigned long long seed,
+                         float* scale, float* inv_scale, int* status, void* stream);
+/* spectral.block_seed (spectral.py:53-55), host side. */
+unsigned long long dash_block_seed(unsigned long long seed, unsigned long long index);
+/* First `count` draws of default_rng(seed).uniform(-1, 1), computed on the device (double). */
+int dash_uniform_pm1(unsigned long long seed, int count, double* out, void* stream);
 
 #ifdef __cplusplus
 }

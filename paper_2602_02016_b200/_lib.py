@@ -32,7 +32,16 @@ class dash_stack(ctypes.Structure):
     ]
 
 
+class dash_block(ctypes.Structure):
+    _fields_ = [
+        ("off", c_longlong), ("ld", c_int), ("rows", c_int), ("cols", c_int),
+        ("group_l", c_int), ("slot_l", c_int), ("group_r", c_int), ("slot_r", c_int),
+    ]
+
+
 _P = ctypes.POINTER(dash_stack)
+_PB = ctypes.POINTER(dash_block)
+c_ull = ctypes.c_ulonglong
 
 # name -> (restype, argtypes); mirrors include/dash_b200.h
 _SIGNATURES: dict[str, tuple] = {
@@ -43,6 +52,33 @@ _SIGNATURES: dict[str, tuple] = {
     "dash_bmm_ws_bytes": (c_size_t, [c_int]),
     "dash_bmm": (c_int, [_P, c_int, _P, c_int, _P, c_void_p, c_longlong, c_int, c_float, c_int, c_void_p,
                          c_size_t, c_void_p]),
+    "dash_ndb_ws_bytes": (c_size_t, [c_int, c_int]),
+    "dash_ndb": (c_int, [_P, c_void_p, _P, _P, c_float, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
+                         c_size_t, c_void_p]),
+    "dash_cn_ws_bytes": (c_size_t, [c_int, c_int]),
+    "dash_cn": (c_int, [_P, c_void_p, c_int, c_float, _P, c_float, c_int, c_int, c_void_p, c_void_p, c_void_p,
+                        c_void_p, c_size_t, c_void_p]),
+    "dash_scale_stack": (c_int, [_P, c_void_p, c_float, c_void_p, c_longlong, c_int, _P, c_void_p]),
+    "dash_cheb_ws_bytes": (c_size_t, [c_int, c_int]),
+    "dash_clenshaw": (c_int, [_P, c_void_p, c_void_p, c_void_p, c_int, c_void_p, _P, c_int, c_void_p, c_size_t,
+                              c_void_p]),
+    "dash_plan_ws_bytes": (c_size_t, [c_int, c_int]),
+    "dash_plan_create": (c_void_p, [_PB, c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p, _P,
+                                    c_void_p, c_void_p, c_void_p, _P, _P, _P, c_void_p, c_void_p, c_void_p,
+                                    c_void_p, c_void_p, c_void_p, c_float, c_int, c_void_p, c_size_t, c_void_p,
+                                    ctypes.POINTER(c_int)]),
+    "dash_plan_destroy": (None, [c_void_p]),
+    "dash_plan_un_stride": (c_int, [c_void_p]),
+    "dash_prep_parts": (c_int, []),
+    "dash_plan_accumulate": (c_int, [c_void_p, c_float, c_float, c_int, c_float, c_void_p]),
+    "dash_plan_apply": (c_int, [c_void_p, c_void_p, c_void_p, c_float, c_void_p]),
+    "dash_group_sym": (c_int, [c_void_p, c_int, c_int, c_float, c_void_p, c_void_p, c_void_p]),
+    "dash_group_split_a": (c_int, [c_void_p, c_float, _P, c_void_p]),
+    "dash_fro_scale": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
+    "dash_power_iteration": (c_int, [c_void_p, c_int, c_int, c_float, c_int, c_int, c_ull, c_void_p, c_void_p,
+                                     c_void_p, c_void_p]),
+    "dash_block_seed": (c_ull, [c_ull, c_ull]),
+    "dash_uniform_pm1": (c_int, [c_ull, c_int, c_void_p, c_void_p]),
 }
 
 

@@ -147,12 +147,12 @@ int JobBuilder::add_map(const dash_stack& s, int box_rows) {
 
 // Fill operand fields of `j` for C = op(A) op(B); returns false on a shape mismatch or map failure.
 bool JobBuilder::operands(GemmJob& j, const dash_stack& a, int am, int trans_a, const dash_stack& b, int bm,
-                          int trans_b) {
+                          int trans_b, bool check) {
   const int M = trans_a ? a.cols : a.rows;
   const int K = trans_a ? a.rows : a.cols;
   const int Kb = trans_b ? b.cols : b.rows;
   const int N = trans_b ? b.rows : b.cols;
-  if (K != Kb) return false;
+  if (check && K != Kb) return false;
   std::memset(&j, 0, sizeof(j));
   j.a_mn = trans_a ? 1 : 0;  // stored K x M -> MN-major
   j.b_mn = trans_b ? 0 : 1;  // stored K x N -> MN-major; stored N x K -> K-major
@@ -189,6 +189,44 @@ void JobBuilder::push(GemmJob& j) {
 
 size_t JobBuilder::bytes_for(int nmaps, int njobs) {
   return static_cast<size_t>(nmaps) * sizeof(CUtensorMap) + static_cast<size_t>(njobs) * sizeof(GemmJob) + 256;
+}
+
+bool JobBuilder::upload(Arena& ar, cudaStream_t st, UploadedGemm* out) {
+  *out = UploadedGemm{};
+  if (jobs.empty()) return true;
+  const size_t mb = maps.size() * sizeof(CUtensorMap), jb = jobs.size() * sizeof(GemmJob);
+  uint8_t* d = static_cast<uint8_t*>(ar.take(mb + jb));
+  if (!d) return false;
+  staging.resize(mb + jb);
+  std::memcpy(staging.data(), maps.data(), mb);
+  std::memcpy(staging.data() + mb, jobs.data(), jb);
+  if (cudaMemcpyAsync(d, staging.data(), mb + jb, cudaMemcpyHostToDevice, st) != cudaSuccess) return false;
+  out->maps = reinterpret_cast<const CUtensorMap*>(d);
+  out->jobs = reinterpret_cast<const GemmJob*>(d + mb);
+  out->njobs = static_cast<int>(jobs.size());
+  out->tiles = tiles;
+  return true;
+}
+
+size_t stack_bytes(int nmat, int rows, int cols) {
+  const int ld = (cols + kLdAlign - 1) / kLdAlign * kLdAlign;
+  return Arena::need(static_cast<size_t>(nmat) * 2 * rows * ld * 2) + 2 * Arena::need(sizeof(int) * nmat);
+}
+
+bool arena_stack(Arena& ar, const dash_stack& like, dash_stack* out) {
+  *out = like;
+  out->ld = (like.cols + kLdAlign - 1) / kLdAlign * kLdAlign;
+  out->data = static_cast<uint16_t*>(ar.take(static_cast<size_t>(like.nmat) * 2 * like.rows * out->ld * 2));
+  out->exp = ar.take_n<int>(like.nmat);
+  out->amax = ar.take_n<uint32_t>(like.nmat);
+  return ar.ok;
+}
+
+void zero_padding(const dash_stack& s, cudaStream_t st) {
+  // K-major TMA loads read the padding columns [cols, ld): they must hold zeros.
+  if (s.cols == s.ld) return;
+  cudaMemset2DAsync(reinterpret_cast<uint16_t*>(s.data) + s.cols, static_cast<size_t>(s.ld) * 2, 0,
+                    static_cast<size_t>(s.ld - s.cols) * 2, static_cast<size_t>(s.nmat) * 2 * s.rows, st);
 }
 
 int JobBuilder::launch(void* ws, size_t ws_bytes, int passes, cudaStream_t st) {

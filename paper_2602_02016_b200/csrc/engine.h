@@ -16,7 +16,38 @@ bool stack_ok(const dash_stack* s);
 int split_stack(const float* src, long long mat_stride, int src_ld, const dash_stack& d, cudaStream_t st);
 int unsplit_stack(const dash_stack& s, float* dst, long long mat_stride, int dst_ld, cudaStream_t st);
 int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtensorMap* d_maps, int passes,
-                cudaStream_t stream);
+                cudaStream_t stream, const int* gate = nullptr);
+
+// A grouped GEMM whose maps + jobs already live in device memory.
+struct UploadedGemm {
+  const GemmJob* jobs = nullptr;
+  const CUtensorMap* maps = nullptr;
+  int njobs = 0, tiles = 0;
+  int run(int passes, cudaStream_t st, const int* gate = nullptr) const {
+    return njobs ? gemm_launch(jobs, njobs, tiles, maps, passes, st, gate) : 0;
+  }
+};
+
+// Bump allocator over a caller-owned workspace (128-byte aligned slices).
+struct Arena {
+  uint8_t* base = nullptr;
+  size_t cap = 0, used = 0;
+  bool ok = true;
+  Arena(void* p, size_t n) : base(static_cast<uint8_t*>(p)), cap(n) {}
+  void* take(size_t n) {
+    size_t off = (used + 127) & ~size_t(127);
+    if (!base || off + n > cap) { ok = false; return nullptr; }
+    used = off + n;
+    return base + off;
+  }
+  template <class T> T* take_n(size_t count) { return static_cast<T*>(take(count * sizeof(T))); }
+  static size_t need(size_t n) { return ((n + 127) & ~size_t(127)); }
+};
+
+// Split stack carved from an arena (same nmat/rows/cols as `like`).
+bool arena_stack(Arena& ar, const dash_stack& like, dash_stack* out);
+size_t stack_bytes(int nmat, int rows, int cols);
+void zero_padding(const dash_stack& s, cudaStream_t st);
 
 // Collects tensor maps + jobs of one grouped GEMM launch and uploads them into a workspace.
 struct JobBuilder {
@@ -37,11 +68,16 @@ struct JobBuilder {
     tiles = 0;
   }
   int add_map(const dash_stack& s, int box_rows);
-  bool operands(GemmJob& j, const dash_stack& a, int am, int trans_a, const dash_stack& b, int bm, int trans_b);
+  // check = false: the caller overrides M/N/K afterwards (sub-matrices of zero-padded slots)
+  bool operands(GemmJob& j, const dash_stack& a, int am, int trans_a, const dash_stack& b, int bm, int trans_b,
+                bool check = true);
   void set_out(GemmJob& j, const dash_stack& c, int cm);
   void push(GemmJob& j);
   static size_t bytes_for(int nmaps, int njobs);
   int launch(void* ws, size_t ws_bytes, int passes, cudaStream_t st);
+  // Upload maps + jobs into the arena (one H2D copy); the builder may be reused afterwards.
+  bool upload(Arena& ar, cudaStream_t st, UploadedGemm* out);
+  size_t upload_bytes() const { return bytes_for(static_cast<int>(maps.size()), static_cast<int>(jobs.size())); }
 };
 
 }  // namespace dash

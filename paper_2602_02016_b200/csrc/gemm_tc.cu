@@ -122,8 +122,9 @@ __device__ __forceinline__ void load_split32(const __half* hi, long long plane, 
 template <int PASSES>
 __global__ void __launch_bounds__(192, 1)
     dash_gemm_kernel(const GemmJob* __restrict__ jobs, int njobs, int total_tiles,
-                     const CUtensorMap* __restrict__ maps) {
+                     const CUtensorMap* __restrict__ maps, const int* __restrict__ gate) {
   using C = GemmCfg<PASSES>;
+  if (gate && *gate == 0) return;  // nothing active (uniform across the grid)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
@@ -250,6 +251,7 @@ __global__ void __launch_bounds__(192, 1)
       const float sc = ldexpf(1.f, ea + eb);
       float mul = jb.alpha * (jb.alpha_p ? __ldg(jb.alpha_p + mat) : 1.f);
       const bool inactive = jb.active && __ldg(jb.active + mat) == 0;
+      const float gam = jb.gamma_p ? *jb.gamma_p : jb.gamma;
       // output exponent
       const float prod_bound = static_cast<float>(jb.K) * amax_of(jb.a_amax) * amax_of(jb.b_amax);
       int e_out = 0, e_side = 0;
@@ -262,10 +264,10 @@ __global__ void __launch_bounds__(192, 1)
         case EPI_SPLIT: e_out = exp_from_bound(prod_bound * fabsf(mul)); break;
         case EPI_NDB_E: e_out = kEExp; break;
         case EPI_CHEB:
-          e_out = exp_from_bound(2.f * prod_bound + amax_of(jb.s_amax) + fabsf(jb.gamma));
+          e_out = exp_from_bound(2.f * prod_bound + amax_of(jb.s_amax) + fabsf(gam));
           break;
         case EPI_CHEB_FINAL:
-          e_out = exp_from_bound((prod_bound + amax_of(jb.s_amax) + fabsf(jb.gamma)) * fabsf(mul));
+          e_out = exp_from_bound((prod_bound + amax_of(jb.s_amax) + fabsf(gam)) * fabsf(mul));
           break;
         case EPI_CN_M: e_out = exp_from_bound(prod_bound); break;
         default: break;
@@ -348,7 +350,7 @@ __global__ void __launch_bounds__(192, 1)
             const bool fin = op == EPI_CHEB_FINAL;
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
-              const float d = (r == c0 + i) ? jb.gamma : 0.f;
+              const float d = (r == c0 + i) ? gam : 0.f;
               float x = fin ? (v[i] * sc - s[i] + d) * mul : 2.f * (v[i] * sc) - s[i] + d;
               v[i] = x;
               if (row_ok && c0 + i < jb.N) amax_loc = nonneg_max(amax_loc, fabsf(x));
@@ -417,7 +419,7 @@ __global__ void __launch_bounds__(192, 1)
 static int g_num_sms = 0;
 
 int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtensorMap* d_maps, int passes,
-                cudaStream_t stream) {
+                cudaStream_t stream, const int* gate) {
   if (total_tiles <= 0) return 0;
   if (g_num_sms == 0) {
     int dev = 0;
@@ -432,14 +434,14 @@ int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtenso
       cudaFuncSetAttribute(dash_gemm_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<3>::kSmemBytes);
       attr = true;
     }
-    dash_gemm_kernel<3><<<grid, 192, GemmCfg<3>::kSmemBytes, stream>>>(d_jobs, njobs, total_tiles, d_maps);
+    dash_gemm_kernel<3><<<grid, 192, GemmCfg<3>::kSmemBytes, stream>>>(d_jobs, njobs, total_tiles, d_maps, gate);
   } else {
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(dash_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<1>::kSmemBytes);
       attr = true;
     }
-    dash_gemm_kernel<1><<<grid, 192, GemmCfg<1>::kSmemBytes, stream>>>(d_jobs, njobs, total_tiles, d_maps);
+    dash_gemm_kernel<1><<<grid, 192, GemmCfg<1>::kSmemBytes, stream>>>(d_jobs, njobs, total_tiles, d_maps, gate);
   }
   err = cudaGetLastError();
   return err == cudaSuccess ? 0 : 3;

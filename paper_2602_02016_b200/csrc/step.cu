@@ -1,0 +1,632 @@
+// Optimizer-step kernels: gradient prep (Adam / momentum EMA + graft-direction norms + block max),
+// gradient blocking into split stacks, preconditioner symmetrization, pooled power iteration,
+// and the grafted parameter update.  Plus the `dash_plan` that owns the per-structure GEMM job
+// tables (statistics EMA and the L^(-1/4) G R^(-1/4) apply) so a step launches a fixed set of kernels.
+//
+// Reference: shampoo.py:238-278 (accumulate), :294-298 (_group_scales), :352-404 (graft_scale, step),
+// spectral.py:53-117 (block_seed, start vectors, pooled power iteration).
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "engine.h"
+#include "ptx.cuh"
+#include "rng.cuh"
+
+namespace dash {
+
+constexpr int kPrepParts = 16;  // CTAs per block in the elementwise passes (fixed -> deterministic sums)
+
+__device__ __forceinline__ int exp_for_amax(float amax) {
+  if (!(amax > 0.f) || !(amax < 3.0e38f)) return 0;
+  int x;
+  frexpf(amax, &x);
+  return x - 15;
+}
+
+template <int NT>
+__device__ double block_sum_d(double v, double* sh) {
+  v = warp_sum_d(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < NT / 32; ++i) t += sh[i];  // fixed order
+  __syncthreads();
+  return t;
+}
+
+// ---------------------------------------------------------------------------- gradient prep
+// adam <- b2 adam + (1-b2) g^2 ; mom <- b1 mom + (1-b1) g ; P = num / (eps + sqrt(adam * bc2_inv))
+// with num = g (b1 == 0) or mom * bc1_inv; per-block partial sum(P^2) and max|g|.
+__global__ void __launch_bounds__(256) prep_kernel(const dash_block* __restrict__ blocks, const float* __restrict__ g,
+                                                   float* __restrict__ adam, float* __restrict__ mom, float beta2,
+                                                   float beta1, float bc1_inv, float bc2_inv, float geps,
+                                                   float* __restrict__ pn_part, unsigned* __restrict__ gamax) {
+  __shared__ double sh[8];
+  const int b = blockIdx.y, p = blockIdx.x;
+  const dash_block blk = blocks[b];
+  const long long total = static_cast<long long>(blk.rows) * blk.cols;
+  const long long per = (total + kPrepParts - 1) / kPrepParts;
+  const long long e0 = p * per, e1 = min(total, e0 + per);
+  double pn = 0.0;
+  float mx = 0.f;
+  for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+    const int r = static_cast<int>(e / blk.cols), c = static_cast<int>(e % blk.cols);
+    const long long i = blk.off + static_cast<long long>(r) * blk.ld + c;
+    const float gv = g[i];
+    const float a = beta2 * adam[i] + (1.f - beta2) * gv * gv;
+    adam[i] = a;
+    float num = gv;
+    if (mom) {
+      const float m = beta1 * mom[i] + (1.f - beta1) * gv;
+      mom[i] = m;
+      num = m * bc1_inv;
+    }
+    const float pv = num / (geps + sqrtf(a * bc2_inv));
+    pn += static_cast<double>(pv) * pv;
+    float av = fabsf(gv);
+    if (!(av <= 3.0e38f)) av = __uint_as_float(0x7fc00000u);
+    mx = nonneg_max(mx, av);
+  }
+  const double t = block_sum_d<256>(pn, sh);
+  if (threadIdx.x == 0) pn_part[b * kPrepParts + p] = static_cast<float>(t);
+  mx = warp_max_nonneg(mx);
+  if ((threadIdx.x & 31) == 0) atomic_max_nonneg(gamax + b, mx);
+}
+
+// Copy block b of the flat gradient into slot b of a split stack (zero padded), exponent from max|g|.
+__global__ void __launch_bounds__(256) grad_split_kernel(const dash_block* __restrict__ blocks,
+                                                         const float* __restrict__ g, dash_stack st,
+                                                         const unsigned* __restrict__ gamax) {
+  const int b = blockIdx.y;
+  const dash_block blk = blocks[b];
+  const float amax = __uint_as_float(gamax[b]);
+  const int e = exp_for_amax(amax);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st.exp[b] = e;
+    st.amax[b] = gamax[b];
+  }
+  const float inv = ldexpf(1.f, -e);
+  __half* hi = reinterpret_cast<__half*>(st.data) + static_cast<long long>(b) * 2 * st.rows * st.ld;
+  __half* lo = hi + static_cast<long long>(st.rows) * st.ld;
+  const long long total = static_cast<long long>(st.rows) * st.ld;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(i / st.ld), c = static_cast<int>(i % st.ld);
+    float y = 0.f;
+    if (r < blk.rows && c < blk.cols) y = g[blk.off + static_cast<long long>(r) * blk.ld + c] * inv;
+    const __half h = __float2half_rn(y);
+    hi[i] = h;
+    lo[i] = __float2half_rn(y - __half2float(h));
+  }
+}
+
+// ---------------------------------------------------------------------------- preconditioner stats
+// In-place symmetrization ema <- (ema + ema^T) / 2 of an (n, d, d) stack (linalg.symmetrize), plus
+// per-block max|a| and sum(a^2) partials of a = ema + eps I (inputs of the solver split / Frobenius scale).
+__global__ void __launch_bounds__(256) sym_kernel(float* __restrict__ ema, int d, float eps,
+                                                  unsigned* __restrict__ amax, float* __restrict__ fro_part) {
+  __shared__ double sh[8];
+  const int m = blockIdx.y, p = blockIdx.x;
+  float* a = ema + static_cast<long long>(m) * d * d;
+  const long long total = static_cast<long long>(d) * d;
+  const long long per = (total + kPrepParts - 1) / kPrepParts;
+  const long long e0 = p * per, e1 = min(total, e0 + per);
+  double fro = 0.0;
+  float mx = 0.f;
+  for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+    const int r = static_cast<int>(e / d), c = static_cast<int>(e % d);
+    if (r < c) {
+      const long long o1 = static_cast<long long>(r) * d + c, o2 = static_cast<long long>(c) * d + r;
+      const float v = (a[o1] + a[o2]) * 0.5f;
+      a[o1] = v;
+      a[o2] = v;
+      fro += 2.0 * static_cast<double>(v) * v;
+      mx = nonneg_max(mx, fabsf(v));
+    } else if (r == c) {
+      const float v = a[static_cast<long long>(r) * d + c] + eps;
+      fro += static_cast<double>(v) * v;
+      mx = nonneg_max(mx, fabsf(v));
+    }
+  }
+  const double t = block_sum_d<256>(fro, sh);
+  if (threadIdx.x == 0) fro_part[m * kPrepParts + p] = static_cast<float>(t);
+  mx = warp_max_nonneg(mx);
+  if ((threadIdx.x & 31) == 0) atomic_max_nonneg(amax + m, mx);
+}
+
+// a = ema + eps I -> split stack (exponent from the exact max computed by sym_kernel).
+__global__ void __launch_bounds__(256) a_split_kernel(const float* __restrict__ ema, float eps, dash_stack st) {
+  const int m = blockIdx.y;
+  const int d = st.rows;
+  const int e = exp_for_amax(__uint_as_float(st.amax[m]));
+  if (blockIdx.x == 0 && threadIdx.x == 0) st.exp[m] = e;
+  const float inv = ldexpf(1.f, -e);
+  const float* a = ema + static_cast<long long>(m) * d * d;
+  __half* hi = reinterpret_cast<__half*>(st.data) + static_cast<long long>(m) * 2 * d * st.ld;
+  __half* lo = hi + static_cast<long long>(d) * st.ld;
+  const long long total = static_cast<long long>(d) * st.ld;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(i / st.ld), c = static_cast<int>(i % st.ld);
+    float v = 0.f;
+    if (c < d) v = a[static_cast<long long>(r) * d + c] + (r == c ? eps : 0.f);
+    const float y = v * inv;
+    const __half h = __float2half_rn(y);
+    hi[i] = h;
+    lo[i] = __float2half_rn(y - __half2float(h));
+  }
+}
+
+// Frobenius scale (shampoo.py:296): s = sqrt(sum a^2), fixed-order reduction of the partials.
+__global__ void fro_scale_kernel(const float* __restrict__ fro_part, int n, float* __restrict__ scale,
+                                 float* __restrict__ inv_scale) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n) return;
+  double t = 0.0;
+  for (int p = 0; p < kPrepParts; ++p) t += fro_part[m * kPrepParts + p];
+  const float s = static_cast<float>(sqrt(t));
+  scale[m] = s;
+  inv_scale[m] = s > 0.f ? 1.f / s : 0.f;
+}
+
+// ---------------------------------------------------------------------------- power iteration
+// One CTA per block (spectral.py:87-112): pool of `pool` start vectors from default_rng(block_seed(seed, m))
+// uniform(-1, 1) drawn row-per-vector and column-normalized, `iters` x (W = A V, column-normalize,
+// dead columns -> 0), quotients q = diag(V^T A V), best alive column, lambda = q / |v|^2, scale = 2 lambda.
+// A = ema + eps I is read from the fp32 stack (L2-resident across the iterations of one block).
+constexpr int kPiThreads = 512;
+constexpr int kPiPool = 16;
+
+__device__ void pi_matvec(const float* __restrict__ a, int d, float eps, const float* __restrict__ v,
+                          float* __restrict__ w) {
+  // w[r][0..15] = sum_k a[r][k] v[k][0..15]; each warp owns rows r = warp + 16 i, lanes split k.
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r0 = warp * 2; r0 < d; r0 += (kPiThreads / 32) * 2) {
+    float acc[2][kPiPool];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int j = 0; j < kPiPool; ++j) acc[q][j] = 0.f;
+    const bool two = r0 + 1 < d;
+    const float* ar0 = a + static_cast<long long>(r0) * d;
+    const float* ar1 = a + static_cast<long long>(two ? r0 + 1 : r0) * d;
+    for (int k = lane; k < d; k += 32) {
+      float x0 = __ldg(ar0 + k), x1 = __ldg(ar1 + k);
+      if (k == r0) x0 += eps;
+      if (k == r0 + 1) x1 += eps;
+      const float4* vk = reinterpret_cast<const float4*>(v + k * kPiPool);
+#pragma unroll
+      for (int j4 = 0; j4 < kPiPool / 4; ++j4) {
+        const float4 t = vk[j4];
+        acc[0][4 * j4 + 0] += x0 * t.x; acc[0][4 * j4 + 1] += x0 * t.y;
+        acc[0][4 * j4 + 2] += x0 * t.z; acc[0][4 * j4 + 3] += x0 * t.w;
+        acc[1][4 * j4 + 0] += x1 * t.x; acc[1][4 * j4 + 1] += x1 * t.y;
+        acc[1][4 * j4 + 2] += x1 * t.z; acc[1][4 * j4 + 3] += x1 * t.w;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int j = 0; j < kPiPool; ++j) acc[q][j] = warp_sum(acc[q][j]);
+    if (lane < kPiPool) {
+      float o0 = 0.f, o1 = 0.f;
+#pragma unroll
+      for (int j = 0; j < kPiPool; ++j)
+        if (j == lane) { o0 = acc[0][j]; o1 = acc[1][j]; }
+      w[r0 * kPiPool + lane] = o0;
+      if (two) w[(r0 + 1) * kPiPool + lane] = o1;
+    }
+  }
+}
+
+// column sums of f(x) over d rows in fixed order -> out[16] (double), using smem scratch red[32*16]
+__device__ void pi_colsum(const float* __restrict__ x, const float* __restrict__ y, int d, double* red,
+                          double* out) {
+  // thread t: column j = t % 16, row stripe s = t / 16 (32 stripes)
+  const int j = threadIdx.x % kPiPool, s = threadIdx.x / kPiPool;
+  double acc = 0.0;
+  for (int r = s; r < d; r += kPiThreads / kPiPool)
+    acc += static_cast<double>(x[r * kPiPool + j]) * (y ? y[r * kPiPool + j] : x[r * kPiPool + j]);
+  red[s * kPiPool + j] = acc;
+  __syncthreads();
+  if (threadIdx.x < kPiPool) {
+    double t = 0.0;
+    for (int q = 0; q < kPiThreads / kPiPool; ++q) t += red[q * kPiPool + threadIdx.x];
+    out[threadIdx.x] = t;
+  }
+  __syncthreads();
+}
+
+__device__ void pi_start(float* v, int d, int pool, uint64_t seed, double* red, double* nrm) {
+  // row-per-vector draws: element (j, i) is draw number j * d + i of default_rng(seed)
+  const long long total = static_cast<long long>(pool) * d;
+  const long long per = (total + kPiThreads - 1) / kPiThreads;
+  const long long s0 = threadIdx.x * per, s1 = min(total, s0 + per);
+  if (s0 < s1) {
+    rng::Pcg64 g;
+    g.seed(seed);
+    g.advance(static_cast<uint64_t>(s0));
+    for (long long t = s0; t < s1; ++t) {
+      const int j = static_cast<int>(t / d), i = static_cast<int>(t % d);
+      v[i * kPiPool + j] = static_cast<float>(g.uniform_pm1());
+    }
+  }
+  for (long long t = threadIdx.x; t < static_cast<long long>(kPiPool - pool) * d; t += kPiThreads) {
+    const int j = pool + static_cast<int>(t / d), i = static_cast<int>(t % d);
+    v[i * kPiPool + j] = 0.f;
+  }
+  __syncthreads();
+  pi_colsum(v, nullptr, d, red, nrm);
+  for (int t = threadIdx.x; t < d * kPiPool; t += kPiThreads) {
+    const int j = t % kPiPool;
+    double n = sqrt(nrm[j]);
+    if (n == 0.0) n = 1.0;
+    v[t] = static_cast<float>(v[t] / n);
+  }
+  __syncthreads();
+}
+
+__device__ void pi_run(const float* a, int d, float eps, float* v, float* w, int iters, double* red,
+                       double* nrm) {
+  for (int it = 0; it < iters; ++it) {
+    pi_matvec(a, d, eps, v, w);
+    __syncthreads();
+    pi_colsum(w, nullptr, d, red, nrm);
+    for (int t = threadIdx.x; t < d * kPiPool; t += kPiThreads) {
+      const double n = sqrt(nrm[t % kPiPool]);
+      v[t] = n > 0.0 ? static_cast<float>(w[t] / n) : 0.f;
+    }
+    __syncthreads();
+  }
+  pi_matvec(a, d, eps, v, w);  // quotients need A V once more (spectral.py:83)
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kPiThreads, 1) pi_kernel(const float* __restrict__ ema, int d, float eps,
+                                                           int pool, int iters, unsigned long long seed,
+                                                           float* __restrict__ scale, float* __restrict__ inv_scale,
+                                                           int* __restrict__ status) {
+  extern __shared__ float pi_smem[];
+  float* v = pi_smem;                  // d x 16
+  float* w = v + d * kPiPool;          // d x 16
+  __shared__ double red[kPiThreads];
+  __shared__ double nrm[kPiPool], q[kPiPool], vv[kPiPool], anrm;
+  const int m = blockIdx.x;
+  const float* a = ema + static_cast<long long>(m) * d * d;
+  uint64_t bseed = rng::block_seed(seed, static_cast<uint64_t>(m));
+  float lam = 0.f;
+  int st = 0;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    pi_start(v, d, pool, bseed, red, nrm);
+    pi_run(a, d, eps, v, w, iters, red, nrm);
+    pi_colsum(v, w, d, red, q);       // q_j = v_j . (A v_j)
+    pi_colsum(v, nullptr, d, red, vv);  // |v_j|^2 (alive iff > 0)
+    if (threadIdx.x == 0) {
+      int best = -1;
+      double bq = 0.0;
+      bool any = false;
+      for (int j = 0; j < pool; ++j) {
+        if (vv[j] > 0.0) {
+          if (!any || q[j] > bq) { bq = q[j]; best = j; }  // first max wins ties (np.argmax)
+          any = true;
+        }
+      }
+      anrm = (any && bq != 0.0) ? bq / vv[best] : 0.0;
+      nrm[0] = any && bq != 0.0 ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    if (nrm[0] != 0.0) {
+      lam = static_cast<float>(anrm);
+      break;
+    }
+    // collapsed pool: zero matrix -> lambda = 0; otherwise reseed once (spectral.py:99-107)
+    if (attempt == 0) {
+      bseed = rng::block_seed(bseed, 0x5EEDull);
+      st = 1;
+    } else {
+      st = 2;
+    }
+  }
+  if (threadIdx.x == 0) {
+    const float s = 2.f * lam;
+    scale[m] = s;
+    inv_scale[m] = s > 0.f ? 1.f / s : 0.f;
+    if (status) status[m] = (st == 2) ? 2 : (s > 0.f ? 0 : 1);
+  }
+}
+
+// ---------------------------------------------------------------------------- grafted update
+// theta_out = theta_in - eta * s_b * U with s_b = |P_b| / |U_b| (0 if |U_b| = 0) (shampoo.py:352-359, :393).
+__global__ void __launch_bounds__(256) update_kernel(const dash_block* __restrict__ blocks, int nb_m, int bsz,
+                                                     const float* __restrict__ pn_part,
+                                                     const float* __restrict__ un_part, int un_stride,
+                                                     const float* __restrict__ um, const float* __restrict__ uv,
+                                                     const float* __restrict__ theta_in, float* __restrict__ theta_out,
+                                                     float eta, float* __restrict__ graft_s) {
+  const int b = blockIdx.y;
+  const dash_block blk = blocks[b];
+  __shared__ float coef;
+  if (threadIdx.x == 0) {
+    double pn = 0.0, un = 0.0;
+    for (int p = 0; p < kPrepParts; ++p) pn += pn_part[b * kPrepParts + p];
+    const int ntiles = ((blk.rows + kTileM - 1) / kTileM) * ((blk.cols + kTileN - 1) / kTileN) * 4;
+    for (int i = 0; i < ntiles; ++i) un += un_part[static_cast<long long>(b) * un_stride + i];
+    const double s = un == 0.0 ? 0.0 : sqrt(pn) / sqrt(un);
+    coef = static_cast<float>(static_cast<double>(eta) * s);
+    if (graft_s && blockIdx.x == 0) graft_s[b] = static_cast<float>(s);
+  }
+  __syncthreads();
+  const float k = coef;
+  const float* u = b < nb_m ? um + static_cast<long long>(b) * bsz * bsz : uv + static_cast<long long>(b - nb_m) * bsz;
+  const int uld = b < nb_m ? bsz : 1;
+  const long long total = static_cast<long long>(blk.rows) * blk.cols;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(e / blk.cols), c = static_cast<int>(e % blk.cols);
+    const long long i = blk.off + static_cast<long long>(r) * blk.ld + c;
+    theta_out[i] = theta_in[i] - k * u[static_cast<long long>(r) * uld + c];
+  }
+}
+
+// ---------------------------------------------------------------------------- plan
+}  // namespace dash
+
+struct dash_plan {
+  int nb_m = 0, nb_v = 0, bsz = 0, ngroups = 0;
+  std::vector<dash_block> hblocks;  // matrix blocks then vector chunks
+  std::vector<int> gdim, gsize;
+  std::vector<float*> gema;
+  std::vector<dash_stack> groot;
+  dash_block* dblocks = nullptr;
+  float *grad = nullptr, *adam = nullptr, *mom = nullptr, *um = nullptr, *uv = nullptr;
+  float *pn_part = nullptr, *un_part = nullptr, *graft_s = nullptr;
+  unsigned* gamax = nullptr;
+  int un_stride = 0;
+  dash_stack gsm{}, gsv{}, tm{};
+  dash::UploadedGemm g_stats, g_apply1, g_apply2;
+  float beta_lr = 0.95f;
+  int passes = 3;
+};
+
+namespace dash {
+
+static int un_stride_for(int bsz) { return 4 * ((bsz + kTileM - 1) / kTileM) * ((bsz + kTileN - 1) / kTileN); }
+
+static void set_dims(GemmJob& j, int M, int N, int K) {
+  j.M = M;
+  j.N = N;
+  j.K = K;
+  j.tiles_n = (N + kTileN - 1) / kTileN;
+}
+
+static dash_stack slot_stack(const dash_stack& s) { return s; }
+
+size_t plan_ws_bytes(int nb_m, int nb_v) {
+  const int nb = nb_m + nb_v;
+  return Arena::need(sizeof(dash_block) * nb) + JobBuilder::bytes_for(64, 2 * nb) +
+         JobBuilder::bytes_for(64, nb) * 2 + 8192;
+}
+
+}  // namespace dash
+
+using namespace dash;
+
+extern "C" {
+
+size_t dash_plan_ws_bytes(int nb_m, int nb_v) { return plan_ws_bytes(nb_m, nb_v); }
+
+dash_plan* dash_plan_create(const dash_block* blocks, int nb_m, int nb_v, int block_size, int ngroups,
+                            const int* gdim, const int* gsize, float* const* gema, const dash_stack* groot,
+                            float* grad, float* adam, float* mom, const dash_stack* gsm, const dash_stack* gsv,
+                            const dash_stack* tm, float* um, float* uv, float* pn_part, float* un_part,
+                            unsigned* gamax, float* graft_s, float beta_lr, int passes, void* ws, size_t ws_bytes,
+                            void* stream, int* status) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  auto fail = [&](int code) -> dash_plan* {
+    if (status) *status = code;
+    return nullptr;
+  };
+  if (!blocks || nb_m < 0 || nb_v < 0 || nb_m + nb_v == 0 || block_size < 1 || ngroups < 1 || !grad || !adam ||
+      !pn_part || !un_part || !gamax || (passes != 1 && passes != 3))
+    return fail(DASH_EINVAL);
+  if ((nb_m && (!stack_ok(gsm) || !stack_ok(tm) || !um)) || (nb_v && (!stack_ok(gsv) || !uv))) return fail(DASH_EINVAL);
+  dash_plan* p = new dash_plan();
+  p->nb_m = nb_m;
+  p->nb_v = nb_v;
+  p->bsz = block_size;
+  p->ngroups = ngroups;
+  p->hblocks.assign(blocks, blocks + nb_m + nb_v);
+  p->gdim.assign(gdim, gdim + ngroups);
+  p->gsize.assign(gsize, gsize + ngroups);
+  p->gema.assign(gema, gema + ngroups);
+  p->groot.assign(groot, groot + ngroups);
+  p->grad = grad; p->adam = adam; p->mom = mom; p->um = um; p->uv = uv;
+  p->pn_part = pn_part; p->un_part = un_part; p->gamax = gamax; p->graft_s = graft_s;
+  if (nb_m) { p->gsm = *gsm; p->tm = *tm; }
+  if (nb_v) p->gsv = *gsv;
+  p->un_stride = un_stride_for(block_size);
+  p->beta_lr = beta_lr;
+  p->passes = passes;
+  Arena ar(ws, ws_bytes);
+  const int nb = nb_m + nb_v;
+  p->dblocks = ar.take_n<dash_block>(nb);
+  if (!ar.ok) { delete p; return fail(DASH_EINVAL); }
+  cudaMemcpyAsync(p->dblocks, p->hblocks.data(), sizeof(dash_block) * nb, cudaMemcpyHostToDevice, st);
+  // ---- statistics EMA jobs: L = G G^T, R = G^T G per matrix block, L = g g^T per vector chunk
+  JobBuilder js, j1, j2;
+  for (int b = 0; b < nb; ++b) {
+    const dash_block& k = p->hblocks[b];
+    const bool mat = b < nb_m;
+    const dash_stack& gs = mat ? p->gsm : p->gsv;
+    const int sidx = mat ? b : b - nb_m;
+    if (k.group_l < 0 || k.group_l >= ngroups || (mat && (k.group_r < 0 || k.group_r >= ngroups))) {
+      delete p;
+      return fail(DASH_EINVAL);
+    }
+    GemmJob j;
+    // L
+    if (!js.operands(j, gs, sidx, 0, gs, sidx, 1, false)) { delete p; return fail(DASH_EINVAL); }
+    set_dims(j, k.rows, k.rows, k.cols);
+    j.op = EPI_EMA;
+    j.beta = beta_lr;
+    {
+      const int d = p->gdim[k.group_l];
+      j.f_out = p->gema[k.group_l] + static_cast<long long>(k.slot_l) * d * d;
+      j.f_in = j.f_out;
+      j.f_ld = d;
+    }
+    js.push(j);
+    if (mat) {  // R
+      if (!js.operands(j, gs, sidx, 1, gs, sidx, 0, false)) { delete p; return fail(DASH_EINVAL); }
+      set_dims(j, k.cols, k.cols, k.rows);
+      j.op = EPI_EMA;
+      j.beta = beta_lr;
+      const int d = p->gdim[k.group_r];
+      j.f_out = p->gema[k.group_r] + static_cast<long long>(k.slot_r) * d * d;
+      j.f_in = j.f_out;
+      j.f_ld = d;
+      js.push(j);
+    }
+    // ---- apply jobs
+    const dash_stack& rl = p->groot[k.group_l];
+    if (mat) {
+      // T = rootL G_b  (split, into tm slot b)
+      if (!j1.operands(j, rl, k.slot_l, 0, gs, sidx, 0, false)) { delete p; return fail(DASH_EINVAL); }
+      set_dims(j, k.rows, k.cols, k.rows);
+      j.op = EPI_SPLIT;
+      j.out_mat = b;
+      j1.set_out(j, p->tm, b);
+      j1.push(j);
+      // U = T rootR  (fp32 block layout + per-tile sum(U^2))
+      const dash_stack& rr = p->groot[k.group_r];
+      if (!j2.operands(j, p->tm, b, 0, rr, k.slot_r, 0, false)) { delete p; return fail(DASH_EINVAL); }
+      set_dims(j, k.rows, k.cols, k.cols);
+      j.op = EPI_APPLY;
+      j.out_mat = b;
+      j.f_out = p->um + static_cast<long long>(b) * block_size * block_size;
+      j.f_ld = block_size;
+      j.partial = p->un_part + static_cast<long long>(b) * p->un_stride;
+      j2.push(j);
+    } else {
+      // u = rootL g_c (vector chunk)
+      if (!j1.operands(j, rl, k.slot_l, 0, gs, sidx, 0, false)) { delete p; return fail(DASH_EINVAL); }
+      set_dims(j, k.rows, 1, k.rows);
+      j.op = EPI_APPLY;
+      j.out_mat = b;
+      j.f_out = p->uv + static_cast<long long>(sidx) * block_size;
+      j.f_ld = 1;
+      j.partial = p->un_part + static_cast<long long>(b) * p->un_stride;
+      j1.push(j);
+    }
+  }
+  if (!js.upload(ar, st, &p->g_stats) || !j1.upload(ar, st, &p->g_apply1) || !j2.upload(ar, st, &p->g_apply2)) {
+    delete p;
+    return fail(DASH_EINVAL);
+  }
+  if (status) *status = cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ECUDA;
+  return p;
+}
+
+void dash_plan_destroy(dash_plan* p) { delete p; }
+
+// accumulate (shampoo.py:238-278) + graft-direction norms for step index t (n_acc = t + 1).
+int dash_plan_accumulate(dash_plan* p, float beta2, float beta1, int n_acc, float graft_eps, void* stream) {
+  if (!p) return DASH_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int nb = p->nb_m + p->nb_v;
+  const float bc1_inv = p->mom ? static_cast<float>(1.0 / (1.0 - std::pow(static_cast<double>(beta1), n_acc))) : 1.f;
+  const float bc2_inv = static_cast<float>(1.0 / (1.0 - std::pow(static_cast<double>(beta2), n_acc)));
+  cudaMemsetAsync(p->gamax, 0, sizeof(unsigned) * nb, st);
+  prep_kernel<<<dim3(kPrepParts, nb), 256, 0, st>>>(p->dblocks, p->grad, p->adam, p->mom, beta2, beta1, bc1_inv,
+                                                   bc2_inv, graft_eps, p->pn_part, p->gamax);
+  if (p->nb_m)
+    grad_split_kernel<<<dim3(32, p->nb_m), 256, 0, st>>>(p->dblocks, p->grad, p->gsm, p->gamax);
+  if (p->nb_v)
+    grad_split_kernel<<<dim3(4, p->nb_v), 256, 0, st>>>(p->dblocks + p->nb_m, p->grad, p->gsv, p->gamax + p->nb_m);
+  if (int rc = p->g_stats.run(p->passes, st)) return rc;
+  return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ECUDA;
+}
+
+// Symmetrize one group's EMA stack and (optionally) emit a = ema + eps I as a split stack.
+int dash_group_sym(float* ema, int n, int d, float eps, unsigned* amax, float* fro_part, void* stream) {
+  if (!ema || n < 1 || d < 1 || !amax || !fro_part) return DASH_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaMemsetAsync(amax, 0, sizeof(unsigned) * n, st);
+  sym_kernel<<<dim3(kPrepParts, n), 256, 0, st>>>(ema, d, eps, amax, fro_part);
+  return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ECUDA;
+}
+
+int dash_group_split_a(const float* ema, float eps, const dash_stack* a, void* stream) {
+  if (!ema || !stack_ok(a) || a->rows != a->cols) return DASH_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  long long el = static_cast<long long>(a->rows) * a->ld;
+  int gx = static_cast<int>(std::min<long long>(64, std::max<long long>(1, el / 4096)));
+  a_split_kernel<<<dim3(gx, a->nmat), 256, 0, st>>>(ema, eps, *a);
+  return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ECUDA;
+}
+
+int dash_fro_scale(const float* fro_part, int n, float* scale, float* inv_scale, void* stream) {
+  if (!fro_part || n < 1 || !scale || !inv_scale) return DASH_EINVAL;
+  fro_scale_kernel<<<(n + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(fro_part, n, scale, inv_scale);
+  return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ECUDA;
+}
+
+int dash_power_iteration(const float* ema, int n, int d, float eps, int pool, int iters, unsigned long long seed,
+                         float* scale, float* inv_scale, int* status, void* stream) {
+  if (!ema || n < 1 || d < 1 || d > 1024 || pool < 1 || pool > kPiPool || iters < 1 || !scale || !inv_scale)
+    return DASH_EINVAL;
+  const size_t smem = static_cast<size_t>(d) * kPiPool * sizeof(float) * 2;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(pi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * kPiPool * 8);
+    attr = true;
+  }
+  pi_kernel<<<n, kPiThreads, smem, static_cast<cudaStream_t>(stream)>>>(ema, d, eps, pool, iters, seed, scale,
+                                                                        inv_scale, status);
+  return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ECUDA;
+}
+
+// Apply L^(-1/4) G R^(-1/4) (1-D: L^(-1/2) g) and the grafted update theta_out = theta_in - eta s_b U_b.
+int dash_plan_apply(dash_plan* p, const float* theta_in, float* theta_out, float eta, void* stream) {
+  if (!p || !theta_in || !theta_out) return DASH_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (int rc = p->g_apply1.run(p->passes, st)) return rc;
+  if (int rc = p->g_apply2.run(p->passes, st)) return rc;
+  const int nb = p->nb_m + p->nb_v;
+  update_kernel<<<dim3(16, nb), 256, 0, st>>>(p->dblocks, p->nb_m, p->bsz, p->pn_part, p->un_part, p->un_stride,
+                                             p->um, p->uv, theta_in, theta_out, eta, p->graft_s);
+  return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ECUDA;
+}
+
+int dash_plan_un_stride(const dash_plan* p) { return p ? p->un_stride : -1; }
+int dash_prep_parts(void) { return kPrepParts; }
+
+unsigned long long dash_block_seed(unsigned long long seed, unsigned long long index) {
+  return rng::block_seed(seed, index);
+}
+
+// First `count` draws of default_rng(seed).uniform(-1, 1) computed on the device (test hook for the
+// NumPy-compatible stream used by the power iteration).
+__global__ void uniform_kernel(unsigned long long seed, int count, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  rng::Pcg64 g;
+  g.seed(seed);
+  g.advance(static_cast<uint64_t>(i));
+  out[i] = g.uniform_pm1();
+}
+
+int dash_uniform_pm1(unsigned long long seed, int count, double* out, void* stream) {
+  if (count < 0 || !out) return DASH_EINVAL;
+  if (count) uniform_kernel<<<(count + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(seed, count, out);
+  return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ECUDA;
+}
+
+}  // extern "C"

@@ -66,6 +66,7 @@ struct GemmJob {
   // ---- scalars
   float alpha; float beta; float gamma; float pad1;
   const float* alpha_p;   // per-matrix multiplier (indexed by out_mat) or null
+  const float* gamma_p;   // launch-wide scalar overriding gamma (EPI_CHEB: c_k) or null
   unsigned* resid;        // per-matrix residual accumulator (indexed by out_mat) or null
   const int* active;      // per-matrix active flag (indexed by out_mat) or null
   float* partial;         // EPI_APPLY: per-(tile, quarter) partial sums, indexed by local tile

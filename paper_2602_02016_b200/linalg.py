@@ -61,7 +61,9 @@ class SplitStack:
     def __init__(self, nmat: int, rows: int, cols: int, dev: torch.device | None = None):
         dev = dev or device()
         self.rows, self.cols = rows, cols
-        self.data = torch.zeros((nmat, 2, rows, _ld(cols)), dtype=torch.float16, device=dev)
+        ld = _ld(cols)
+        alloc = torch.empty if ld == cols else torch.zeros  # padding columns must be zero (K-major loads)
+        self.data = alloc((nmat, 2, rows, ld), dtype=torch.float16, device=dev)
         self.exp = torch.zeros(nmat, dtype=torch.int32, device=dev)
         self.amax = torch.zeros(nmat, dtype=torch.int32, device=dev)
         self._c = None

@@ -1,0 +1,514 @@
+"""Block-preconditioned Shampoo (DASH) on the B200 — drop-in for the reference ``shampoo.py``.
+
+Same configuration dataclasses, state objects and functions as the reference (``GraftConfig``
+``shampoo.py:53-63``, ``SolverConfig`` ``:66-87``, ``LrSchedule`` ``:90-109``, ``ShampooConfig`` ``:112-130``,
+``SlotRef``/``LayerState``/``PrecondGroup``/``ShampooState`` ``:133-168``, ``init_state`` ``:233``,
+``accumulate`` ``:238``, ``refresh_inverse_roots`` ``:312``, ``graft_scale`` ``:352``, ``step`` ``:362``), with
+identical block structure, group/slot indexing, seeds and update rule.  All state lives on the GPU:
+
+* one flat fp32 parameter space (grad / Adam / momentum / theta) with per-layer views,
+* per group an fp32 EMA stack ``ema`` (n, d, d), fp32 ``roots`` and a split-f16 copy of the roots,
+* a ``dash_plan`` (C ABI) holding the grouped-GEMM job tables of the statistics EMA and the apply.
+
+A step is: gradient prep (Adam EMA, graft-direction norms) -> blocked split of G -> one grouped
+tcgen05 launch for every L/R statistic -> per group symmetrize / scale (Frobenius or pooled power
+iteration) / batched solver (NDB, CN, Chebyshev; EVD comparator) / root rescale -> two grouped launches
+for U = L^(-1/4) G R^(-1/4) -> the grafted update.  NumPy inputs are accepted and returned (the
+reference's types); CUDA tensors stay on the device.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Any
+
+import numpy as np
+import torch
+
+from . import _lib
+from .blocking import PartitionLayout, chunk_bounds, partition_layout
+from .chebyshev import ChebCoefficients, clenshaw_split, fit_inverse_root
+from .eigensolver import DampeningHeuristic, HeuristicKind, evd_inverse_root_torch
+from .errors import ConvergenceError, DegenerateSpectrumError
+from .linalg import PrecisionMode, SplitStack, device, passes_for, workspace
+from .roots import CnConfig, DeviceReports, cn_split, ndb_split
+from .spectral import Frobenius, PowerIterationScaling, ScalingMode, block_seed, power_iteration_scales
+
+SOLVER_METHODS = ("evd", "cn", "ndb", "cbshv")
+
+
+@dataclass(frozen=True)
+class GraftConfig:
+    beta1: float = 0.0
+    beta2: float = 0.999
+    graft_eps: float = 1e-8
+
+    def __post_init__(self) -> None:
+        if not 0.0 <= self.beta1 < 1.0 or not 0.0 <= self.beta2 < 1.0:
+            raise ValueError("betas must lie in [0, 1)")
+        if self.graft_eps <= 0:
+            raise ValueError("graft_eps must be positive")
+
+
+@dataclass(frozen=True)
+class SolverConfig:
+    """Solver selection (shampoo.py:66-87).
+
+    Difference from the reference: Newton-DB accepts every B200 precision mode (the reference allows
+    FULL64 only, shampoo.py:81-82); on the B200 FULL64 and EMULATED32 both run split-f16 products.
+    """
+
+    method: str = "ndb"
+    scaling: ScalingMode = PowerIterationScaling()
+    tolerance: float = 1e-10
+    max_iters: int = 100
+    precision: PrecisionMode = PrecisionMode.FULL64
+    heuristic: DampeningHeuristic = DampeningHeuristic(HeuristicKind.SHIFTED_RELU)
+    cheb_degree: int = 60
+    cheb_points: int = 1000
+    cheb_interval: tuple[float, float] | None = None
+
+    def __post_init__(self) -> None:
+        if self.method not in SOLVER_METHODS:
+            raise ValueError(f"unknown solver method {self.method!r}")
+        if self.max_iters < 1:
+            raise ValueError("max_iters must be >= 1")
+        if self.tolerance < 0:
+            raise ValueError("tolerance must be >= 0")
+
+    @property
+    def require_convergence(self) -> bool:
+        return self.tolerance > 0.0
+
+
+@dataclass(frozen=True)
+class LrSchedule:
+    kind: str = "constant"
+    base: float = 1e-3
+    total_steps: int = 0
+    final: float = 0.0
+
+    def __post_init__(self) -> None:
+        if self.kind not in ("constant", "linear", "cosine"):
+            raise ValueError(f"unknown schedule {self.kind!r}")
+        if self.kind != "constant" and self.total_steps < 1:
+            raise ValueError("linear/cosine schedules need total_steps >= 1")
+
+    def value(self, t: int) -> float:
+        if self.kind == "constant":
+            return self.base
+        frac = min(t / self.total_steps, 1.0)
+        if self.kind == "linear":
+            return self.base + (self.final - self.base) * frac
+        return self.final + (self.base - self.final) * 0.5 * (1.0 + math.cos(math.pi * frac))
+
+
+@dataclass(frozen=True)
+class ShampooConfig:
+    beta_lr: float = 0.95
+    epsilon: float = 1e-10
+    lr: LrSchedule = LrSchedule()
+    update_freq: int = 1
+    solver: SolverConfig = SolverConfig()
+    block_size: int = 256
+    graft: GraftConfig = GraftConfig()
+
+    def __post_init__(self) -> None:
+        if not 0.0 < self.beta_lr < 1.0:
+            raise ValueError("beta_lr must lie in (0, 1)")
+        if self.epsilon <= 0:
+            raise ValueError("epsilon must be positive")
+        if self.update_freq < 1:
+            raise ValueError("update_freq must be >= 1")
+        if self.block_size < 1:
+            raise ValueError("block_size must be >= 1")
+
+
+@dataclass(frozen=True)
+class SlotRef:
+    group: int
+    slot: int
+
+
+@dataclass
+class LayerState:
+    layer_id: int
+    shape: tuple[int, ...]
+    layout: PartitionLayout | None
+    chunk_bounds: tuple[tuple[int, int], ...] | None
+    left_refs: tuple[SlotRef, ...]
+    right_refs: tuple[SlotRef, ...] | None
+
+    @property
+    def is_matrix(self) -> bool:
+        return self.layout is not None
+
+
+@dataclass
+class PrecondGroup:
+    dim: int
+    exponent: int
+    members: tuple[tuple[int, str, int], ...]
+    ema: torch.Tensor     # (n, dim, dim) fp32, CUDA
+    roots: torch.Tensor   # (n, dim, dim) fp32, CUDA
+
+
+@dataclass
+class ShampooState:
+    step: int
+    layers: list[LayerState]
+    groups: list[PrecondGroup]
+    adam: list[torch.Tensor]
+    momentum: list[torch.Tensor] | None
+    runtime: Any = field(default=None, repr=False)
+
+
+def _chunk_bounds(length: int, block_size: int) -> tuple[tuple[int, int], ...]:
+    return chunk_bounds(length, block_size)
+
+
+# ============================================================================ structure
+def _group_keys(shapes, block_size):
+    keyed: dict[tuple[int, int], list[tuple[int, str, int]]] = {}
+    meta = []
+    for layer_id, shape in enumerate(shapes):
+        if len(shape) == 2:
+            layout = partition_layout(shape, block_size)
+            meta.append((layout, None))
+            for idx, ((r0, r1), (c0, c1)) in enumerate(layout.block_spans):
+                keyed.setdefault((r1 - r0, 4), []).append((layer_id, "L", idx))
+                keyed.setdefault((c1 - c0, 4), []).append((layer_id, "R", idx))
+        elif len(shape) == 1:
+            bounds = _chunk_bounds(shape[0], block_size)
+            meta.append((None, bounds))
+            for idx, (s, e) in enumerate(bounds):
+                keyed.setdefault((e - s, 2), []).append((layer_id, "L", idx))
+        else:
+            raise ValueError(f"layer {layer_id}: only 1-D and 2-D layers are supported, got shape {shape}")
+    return keyed, meta
+
+
+@dataclass(frozen=True)
+class GroupSpec:
+    """Host-side description of one preconditioner group (no device data)."""
+
+    dim: int
+    exponent: int
+    members: tuple[tuple[int, str, int], ...]
+
+
+def build_layout(shapes, block_size: int) -> tuple[list[LayerState], list[GroupSpec]]:
+    """Pure-host block structure: layers with slot refs + groups (shampoo.py:176-230), bit-exact."""
+    keyed, meta = _group_keys([tuple(s) for s in shapes], block_size)
+    side_order = {"L": 0, "R": 1}
+    specs: list[GroupSpec] = []
+    ref_of: dict[tuple[int, str, int], SlotRef] = {}
+    for gi, (dim, exponent) in enumerate(sorted(keyed)):
+        members = tuple(sorted(keyed[(dim, exponent)], key=lambda m: (m[0], side_order[m[1]], m[2])))
+        for slot, member in enumerate(members):
+            ref_of[member] = SlotRef(group=gi, slot=slot)
+        specs.append(GroupSpec(dim, exponent, members))
+    layers = []
+    for layer_id, shape in enumerate(shapes):
+        layout, bounds = meta[layer_id]
+        if layout is not None:
+            nb = layout.num_blocks
+            left = tuple(ref_of[(layer_id, "L", i)] for i in range(nb))
+            right = tuple(ref_of[(layer_id, "R", i)] for i in range(nb))
+            layers.append(LayerState(layer_id, tuple(shape), layout, None, left, right))
+        else:
+            left = tuple(ref_of[(layer_id, "L", i)] for i in range(len(bounds)))
+            layers.append(LayerState(layer_id, tuple(shape), None, bounds, left, None))
+    return layers, specs
+
+
+def _build_structure(shapes: list[tuple[int, ...]], block_size: int, track_momentum: bool) -> ShampooState:
+    """Host structure + device state: EMA zeros, identity roots, flat Adam / momentum (shampoo.py:176-230)."""
+    layers, specs = build_layout(shapes, block_size)
+    dev = device()
+    groups: list[PrecondGroup] = []
+    for sp in specs:
+        n = len(sp.members)
+        roots = torch.zeros((n, sp.dim, sp.dim), dtype=torch.float32, device=dev)
+        roots.diagonal(dim1=1, dim2=2).fill_(1.0)
+        groups.append(PrecondGroup(dim=sp.dim, exponent=sp.exponent, members=sp.members,
+                                   ema=torch.zeros((n, sp.dim, sp.dim), dtype=torch.float32, device=dev),
+                                   roots=roots))
+    state = ShampooState(step=0, layers=layers, groups=groups, adam=[], momentum=None)
+    state.runtime = _Runtime(state, [tuple(s) for s in shapes], block_size, track_momentum)
+    state.adam = state.runtime.views(state.runtime.adam)
+    state.momentum = state.runtime.views(state.runtime.mom) if track_momentum else None
+    return state
+
+
+def init_state(params, cfg: ShampooConfig) -> ShampooState:
+    shapes = [tuple(p.shape) for p in params]
+    return _build_structure(shapes, cfg.block_size, cfg.graft.beta1 > 0.0)
+
+
+# ============================================================================ device runtime
+class _Runtime:
+    """Flat device buffers + the C-ABI plan for one optimizer structure."""
+
+    def __init__(self, state: ShampooState, shapes, block_size: int, momentum: bool):
+        self.dev = device()
+        self.shapes = shapes
+        self.bsz = block_size
+        self.sizes = [int(np.prod(s)) for s in shapes]
+        self.offsets = np.concatenate([[0], np.cumsum(self.sizes)]).astype(np.int64)
+        total = int(self.offsets[-1])
+        f32 = dict(dtype=torch.float32, device=self.dev)
+        self.grad = torch.zeros(total, **f32)
+        self.adam = torch.zeros(total, **f32)
+        self.mom = torch.zeros(total, **f32) if momentum else None
+        self.theta = torch.zeros(total, **f32)
+        self.theta_out = torch.zeros(total, **f32)
+        # block table: matrix blocks (layer order, canonical block order) then 1-D chunks
+        mats, vecs = [], []
+        for layer in state.layers:
+            base = int(self.offsets[layer.layer_id])
+            if layer.is_matrix:
+                n = layer.shape[1]
+                for idx, ((r0, r1), (c0, c1)) in enumerate(layer.layout.block_spans):
+                    lr, rr = layer.left_refs[idx], layer.right_refs[idx]
+                    mats.append((base + r0 * n + c0, n, r1 - r0, c1 - c0, lr.group, lr.slot, rr.group, rr.slot))
+            else:
+                for idx, (s, e) in enumerate(layer.chunk_bounds):
+                    ref = layer.left_refs[idx]
+                    vecs.append((base + s, 1, e - s, 1, ref.group, ref.slot, -1, -1))
+        self.nb_m, self.nb_v = len(mats), len(vecs)
+        nb = self.nb_m + self.nb_v
+        self.block_rows = mats + vecs
+        Arr = _lib.dash_block * nb
+        self.blocks_c = Arr(*[_lib.dash_block(*b) for b in self.block_rows])
+        self.gsm = SplitStack(self.nb_m, block_size, block_size, self.dev) if self.nb_m else None
+        self.tm = SplitStack(self.nb_m, block_size, block_size, self.dev) if self.nb_m else None
+        self.gsv = SplitStack(self.nb_v, block_size, 1, self.dev) if self.nb_v else None
+        self.um = torch.zeros((max(self.nb_m, 1), block_size, block_size), **f32)
+        self.uv = torch.zeros((max(self.nb_v, 1), block_size), **f32)
+        L = _lib.lib()
+        self.prep_parts = L.dash_prep_parts()
+        self.pn_part = torch.zeros(nb * self.prep_parts, **f32)
+        self.un_stride = 4 * (-(-block_size // 128)) * (-(-block_size // 256))
+        self.un_part = torch.zeros(nb * self.un_stride, **f32)
+        self.gamax = torch.zeros(nb, dtype=torch.int32, device=self.dev)
+        self.graft_s = torch.zeros(nb, **f32)
+        self.root_split = [SplitStack(len(g.members), g.dim, g.dim, self.dev) for g in state.groups]
+        for g, rs in zip(state.groups, self.root_split):
+            rs.load(g.roots)  # identity roots before the first refresh
+        self.groups = state.groups
+        # per-group scratch
+        self.g_amax = [torch.zeros(len(g.members), dtype=torch.int32, device=self.dev) for g in state.groups]
+        self.g_fro = [torch.zeros(len(g.members) * self.prep_parts, **f32) for g in state.groups]
+        self.plan = None
+        self.plan_key = None
+
+    def views(self, flat: torch.Tensor) -> list[torch.Tensor]:
+        return [flat[int(self.offsets[i]):int(self.offsets[i + 1])].view(s) for i, s in enumerate(self.shapes)]
+
+    def ensure_plan(self, cfg: ShampooConfig) -> None:
+        key = (cfg.beta_lr, passes_for(cfg.solver.precision))
+        if self.plan is not None and self.plan_key == key:
+            return
+        self.close()
+        L = _lib.lib()
+        ng = len(self.groups)
+        gdim = (ctypes_int * ng)(*[g.dim for g in self.groups])
+        gsize = (ctypes_int * ng)(*[len(g.members) for g in self.groups])
+        gema = (ctypes_vp * ng)(*[g.ema.data_ptr() for g in self.groups])
+        groot = (_lib.dash_stack * ng)(*[rs.c() for rs in self.root_split])
+        self.plan_ws = workspace(L.dash_plan_ws_bytes(self.nb_m, self.nb_v), self.dev)
+        status = ctypes_int(0)
+        p = L.dash_plan_create(
+            self.blocks_c, self.nb_m, self.nb_v, self.bsz, ng, gdim, gsize, gema, groot,
+            self.grad.data_ptr(), self.adam.data_ptr(), self.mom.data_ptr() if self.mom is not None else None,
+            self.gsm.ref() if self.gsm else None, self.gsv.ref() if self.gsv else None,
+            self.tm.ref() if self.tm else None, self.um.data_ptr(), self.uv.data_ptr(), self.pn_part.data_ptr(),
+            self.un_part.data_ptr(), self.gamax.data_ptr(), self.graft_s.data_ptr(), float(cfg.beta_lr),
+            key[1], self.plan_ws.data_ptr(), self.plan_ws.numel(), _lib.stream_ptr(), ctypes_byref(status))
+        if not p:
+            _lib.check(status.value or _lib.DASH_EINVAL, "dash_plan_create")
+        self.plan = p
+        self.plan_key = key
+
+    def close(self) -> None:
+        if self.plan:
+            _lib.lib().dash_plan_destroy(self.plan)
+            self.plan = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+    # ---- host <-> flat buffers
+    def load(self, flat: torch.Tensor, tensors) -> None:
+        for i, t in enumerate(tensors):
+            if tuple(t.shape) != self.shapes[i]:
+                raise ValueError(f"layer {i}: shape {tuple(t.shape)} != {self.shapes[i]}")
+            dst = flat[int(self.offsets[i]):int(self.offsets[i + 1])]
+            if isinstance(t, torch.Tensor):
+                dst.copy_(t.reshape(-1), non_blocking=True)
+            else:
+                dst.copy_(torch.from_numpy(np.ascontiguousarray(t, dtype=np.float32).reshape(-1)))
+
+
+import ctypes as _ct  # noqa: E402
+
+ctypes_int = _ct.c_int
+ctypes_vp = _ct.c_void_p
+ctypes_byref = _ct.byref
+
+
+# ============================================================================ accumulate
+def accumulate(state: ShampooState, grads, cfg: ShampooConfig) -> ShampooState:
+    """EMA update of every preconditioner block and the Adam second moment (shampoo.py:238-278)."""
+    if len(grads) != len(state.layers):
+        raise ValueError(f"expected {len(state.layers)} gradients, got {len(grads)}")
+    rt: _Runtime = state.runtime
+    for layer, g in zip(state.layers, grads):
+        if tuple(g.shape) != layer.shape:
+            raise ValueError(f"layer {layer.layer_id}: gradient shape {tuple(g.shape)} != {layer.shape}")
+    rt.ensure_plan(cfg)
+    rt.load(rt.grad, grads)
+    n_acc = state.step + 1
+    st = _lib.lib().dash_plan_accumulate(rt.plan, float(cfg.graft.beta2), float(cfg.graft.beta1), n_acc,
+                                         float(cfg.graft.graft_eps), _lib.stream_ptr())
+    _lib.check(st, "dash_plan_accumulate")
+    for gi, g in enumerate(state.groups):  # linalg.symmetrize on every EMA block
+        st = _lib.lib().dash_group_sym(g.ema.data_ptr(), len(g.members), g.dim, float(cfg.epsilon),
+                                       rt.g_amax[gi].data_ptr(), rt.g_fro[gi].data_ptr(), _lib.stream_ptr())
+        _lib.check(st, "dash_group_sym")
+    return state
+
+
+# ============================================================================ refresh
+_cheb_cache: dict[tuple, ChebCoefficients] = {}
+
+
+def _solver_coefficients(solver: SolverConfig, p: int) -> ChebCoefficients:
+    interval = solver.cheb_interval if solver.cheb_interval is not None else (1e-10, 1.0 + 1e-10)
+    key = (p, solver.cheb_degree, solver.cheb_points, interval)
+    if key not in _cheb_cache:
+        _cheb_cache[key] = fit_inverse_root(p, degree=solver.cheb_degree, num_points=solver.cheb_points,
+                                            interval=interval)
+    return _cheb_cache[key]
+
+
+def _check_reports(group: PrecondGroup, reports) -> None:
+    failed = [i for i, r in enumerate(reports) if not r.converged]
+    if failed:
+        details = ", ".join(
+            f"layer {group.members[i][0]} side {group.members[i][1]} block {group.members[i][2]}"
+            f" (residual {reports[i].residual:.3e})" for i in failed)
+        raise ConvergenceError(f"inverse-root solver failed on: {details}")
+
+
+def refresh_inverse_roots(state: ShampooState, cfg: ShampooConfig, seed: int = 0) -> ShampooState:
+    """Recompute cached inverse roots; no-op unless step % update_freq == 0 (shampoo.py:312-349)."""
+    if state.step % cfg.update_freq != 0:
+        return state
+    rt: _Runtime = state.runtime
+    solver = cfg.solver
+    L = _lib.lib()
+    pending: list[tuple[PrecondGroup, list[DeviceReports]]] = []
+    statuses = []
+    for gi, group in enumerate(state.groups):
+        p, n, d = group.exponent, len(group.members), group.dim
+        if solver.method == "evd":
+            group.roots.copy_(evd_inverse_root_torch(group.ema, p, solver.heuristic))
+            rt.root_split[gi].load(group.roots)
+            continue
+        a = SplitStack(n, d, d, rt.dev)
+        a.amax = rt.g_amax[gi]  # exact max|ema + eps I| from dash_group_sym
+        _lib.check(L.dash_group_split_a(group.ema.data_ptr(), float(cfg.epsilon), a.ref(), _lib.stream_ptr()),
+                   "dash_group_split_a")
+        scale = torch.empty(n, dtype=torch.float32, device=rt.dev)
+        inv = torch.empty_like(scale)
+        status = torch.zeros(n, dtype=torch.int32, device=rt.dev)
+        if isinstance(solver.scaling, Frobenius):
+            _lib.check(L.dash_fro_scale(rt.g_fro[gi].data_ptr(), n, scale.data_ptr(), inv.data_ptr(),
+                                        _lib.stream_ptr()), "dash_fro_scale")
+        else:
+            power_iteration_scales(group.ema, cfg.epsilon, solver.scaling.pool, solver.scaling.iters,
+                                   block_seed(seed, gi), scale, inv, status)
+        statuses.append((group, scale, status))
+        mode = solver.precision
+        if solver.method == "cbshv":
+            coeffs = _solver_coefficients(solver, p)
+            clenshaw_split(a, coeffs, inv, inv_pow(inv, p), group.roots, rt.root_split[gi], mode)
+            continue
+        if solver.method == "cn":
+            x, rep = cn_split(a, inv, CnConfig(p=p, tolerance=solver.tolerance, max_iters=solver.max_iters), mode)
+            reps = [rep]
+            src = x
+        else:  # ndb
+            if p == 2:
+                _, src, rep = ndb_split(a, inv, solver.tolerance, solver.max_iters, mode)
+                reps = [rep]
+            else:
+                y1, _, r1 = ndb_split(a, inv, solver.tolerance, solver.max_iters, mode)
+                _, src, r2 = ndb_split(y1, None, solver.tolerance, solver.max_iters, mode)
+                reps = [r1, r2]
+        # roots = Z * scale^(-1/p)  -> fp32 state roots + split copy for the apply
+        _lib.check(L.dash_scale_stack(src.ref(), inv.data_ptr(), 1.0 / p, group.roots.data_ptr(),
+                                      group.roots.stride(0), group.roots.stride(1), rt.root_split[gi].ref(),
+                                      _lib.stream_ptr()), "dash_scale_stack")
+        if solver.require_convergence:
+            pending.append((group, reps))
+    # host checks (one synchronisation per refresh, only when the reference would raise)
+    for group, scale, status in statuses:
+        if bool((status == 2).any()):
+            raise DegenerateSpectrumError("power iteration pool collapsed twice on a nonzero matrix")
+        if bool((scale <= 0).any()):
+            raise ConvergenceError(f"non-positive scale in group of dim {group.dim}")
+    for group, reps in pending:
+        for rep in reps:
+            _check_reports(group, rep.to_list())
+    return state
+
+
+def inv_pow(inv: torch.Tensor, p: int) -> torch.Tensor:
+    """scale^(-1/p) from 1/scale (device; tiny vector)."""
+    return inv.double().pow(1.0 / p).float()
+
+
+# ============================================================================ step
+def graft_scale(u, p) -> float:
+    """Frobenius-norm ratio ||p|| / ||u||; zero when the update vanishes (shampoo.py:352-359)."""
+    if tuple(u.shape) != tuple(p.shape):
+        raise ValueError(f"shape mismatch: {tuple(u.shape)} vs {tuple(p.shape)}")
+    nu = float(np.linalg.norm(np.asarray(u.cpu() if isinstance(u, torch.Tensor) else u, dtype=np.float64)))
+    if nu == 0.0:
+        return 0.0
+    return float(np.linalg.norm(np.asarray(p.cpu() if isinstance(p, torch.Tensor) else p, dtype=np.float64))) / nu
+
+
+def step(state: ShampooState, params, grads, cfg: ShampooConfig, seed: int = 0, *, inplace: bool = False):
+    """One optimizer step; returns updated parameters and the mutated state (shampoo.py:362-404).
+
+    NumPy params -> new float64 NumPy arrays (like the reference).  CUDA tensors -> new fp32 tensors, or
+    the input tensors updated in place when ``inplace=True``.
+    """
+    if len(params) != len(state.layers):
+        raise ValueError(f"expected {len(state.layers)} parameter tensors, got {len(params)}")
+    rt: _Runtime = state.runtime
+    t = state.step
+    accumulate(state, grads, cfg)
+    refresh_inverse_roots(state, cfg, seed=block_seed(seed, t))
+    eta = cfg.lr.value(t)
+    rt.load(rt.theta, params)
+    _lib.check(_lib.lib().dash_plan_apply(rt.plan, rt.theta.data_ptr(), rt.theta_out.data_ptr(), float(eta),
+                                          _lib.stream_ptr()), "dash_plan_apply")
+    state.step = t + 1
+    outs = rt.views(rt.theta_out)
+    is_np = not isinstance(params[0], torch.Tensor)
+    if is_np:
+        host = rt.theta_out.double().cpu().numpy()
+        return [host[int(rt.offsets[i]):int(rt.offsets[i + 1])].reshape(s) for i, s in enumerate(rt.shapes)], state
+    if inplace:
+        for p_, o in zip(params, outs):
+            p_.copy_(o)
+        return list(params), state
+    return [o.clone() for o in outs], state

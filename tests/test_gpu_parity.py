@@ -1,0 +1,206 @@
+"""GPU parity: the B200 kernels (through the C ABI) against the CPU oracle / reference golden vectors.
+
+Tolerances (relative Frobenius, stated per path):
+  split-f16 products (EMULATED32/FULL64 modes)  1e-5 .. 1e-4 on small blocks, see each test.
+Integer / index work (block table, seeds, start vectors) is compared bit-exactly.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import core
+from tests.golden.cases import STEP_CASES, WARM, solver_kwargs, uses_momentum
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU containers skip the whole module
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2602_02016_b200 import chebyshev, linalg, roots, shampoo, spectral  # noqa: E402
+from paper_2602_02016_b200.linalg import PrecisionMode  # noqa: E402
+
+
+def relf(x, y):
+    x, y = np.asarray(x, dtype=np.float64), np.asarray(y, dtype=np.float64)
+    d = np.linalg.norm(y)
+    return np.linalg.norm(x - y) / (d if d > 0 else 1.0)
+
+
+@pytest.mark.parametrize("m,n,k", [(128, 256, 64), (256, 256, 256), (37, 53, 29), (300, 700, 130), (1024, 1024, 1024)])
+@pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False), (True, True)])
+def test_bmm_vs_float64(m, n, k, ta, tb):
+    torch.manual_seed(0)
+    a = torch.randn(3, k if ta else m, m if ta else k, device="cuda")
+    b = torch.randn(3, n if tb else k, k if tb else n, device="cuda")
+    c = linalg.bmm(a, b, PrecisionMode.EMULATED32, trans_a=ta, trans_b=tb)
+    ad = a.double().transpose(1, 2) if ta else a.double()
+    bd = b.double().transpose(1, 2) if tb else b.double()
+    ref = (ad @ bd).cpu().numpy()
+    assert relf(c.cpu().numpy(), ref) < 1e-5  # fp32-class (K <= 1024)
+
+
+def test_bmm_f16_mode():
+    torch.manual_seed(1)
+    a, b = torch.randn(2, 512, 512, device="cuda"), torch.randn(2, 512, 512, device="cuda")
+    c = linalg.bmm(a, b, PrecisionMode.F16)
+    assert relf(c.cpu().numpy(), (a.double() @ b.double()).cpu().numpy()) < 2e-3
+
+
+def test_split_roundtrip_and_exponent():
+    x = torch.randn(4, 70, 130, device="cuda") * torch.tensor([1e-6, 1.0, 1e4, 0.0], device="cuda")[:, None, None]
+    s = linalg.SplitStack.from_float(x)
+    back = s.to_float()
+    for i in range(3):
+        assert relf(back[i].cpu().numpy(), x[i].cpu().numpy()) < 1e-6
+    assert float(back[3].abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("seed", [0, 1, 123456789, 2**64 - 1, 13015481096164472892])
+def test_device_pcg64_matches_numpy(seed):
+    got = spectral.device_uniform(seed, 4096).cpu().numpy()
+    want = np.random.default_rng(seed).uniform(-1.0, 1.0, size=4096)
+    np.testing.assert_array_equal(got, want)
+
+
+def test_power_iteration_vs_golden(golden):
+    g = golden["solvers"]
+    a = g["a"]
+    for i, s in enumerate(g["pi_seeds"].tolist()):
+        est = spectral.batched_multi_power_iteration(a[i:i + 1], 16, 30, 0)  # seed is per call below
+        del est
+    # the reference draws block i's pool from block_seed(seed, i); golden used plain seeds -> compare via
+    # single-block calls whose child seed equals the golden seed is not possible, so check lambda_max bound:
+    lams = np.array([e.lam for e in spectral.batched_multi_power_iteration(a, 16, 30, 7)])
+    true = np.linalg.eigvalsh(a)[:, -1]
+    assert np.all(lams <= true * (1 + 1e-5)) and np.all(lams >= true * 0.99)
+
+
+def test_power_iteration_bitexact_seeds_vs_oracle():
+    rng = np.random.default_rng(3)
+    a = np.stack([core.random_spd(96, c, seed=i, scale=s) for i, (c, s) in enumerate([(10, 0.5), (1e3, 2.0), (50, 1e-3)])])
+    seed = 4242
+    lams = [e.lam for e in spectral.batched_multi_power_iteration(a, 16, 30, seed)]
+    want = [core.multi_power_iteration(a[i], 16, 30, core.block_seed(seed, i)) for i in range(3)]
+    np.testing.assert_allclose(lams, want, rtol=2e-6)
+    del rng
+
+
+@pytest.mark.parametrize("tag,tol,mi", [("fix", 0.0, 10), ("tol5", 1e-5, 100)])
+def test_ndb_vs_oracle(golden, tag, tol, mi):
+    a = golden["solvers"]["a"]
+    y, z, rep = roots.batched_newton_db(a, roots.NdbConfig(tolerance=tol, max_iters=mi))
+    yo, zo, ro = core.batched_newton_db(a, tol, mi)
+    for i in range(a.shape[0]):
+        assert relf(y[i], yo[i]) < 2e-5
+        assert relf(z[i], zo[i]) < 1e-4
+    it_gpu, it_ref = [r.iterations for r in rep], [r.iterations for r in ro]
+    assert all(abs(p - q) <= 1 for p, q in zip(it_gpu, it_ref))
+    assert [r.converged for r in rep] == [r.converged for r in ro]
+
+
+def test_ndb_known_answers():
+    y, z, r = roots.batched_newton_db(np.eye(64)[None], roots.NdbConfig(tolerance=1e-6))
+    assert r[0].iterations == 1 and r[0].converged
+    np.testing.assert_allclose(y[0], np.eye(64), atol=1e-6)
+    y, z, r = roots.batched_newton_db(np.full((1, 1, 1), 0.25), roots.NdbConfig(tolerance=1e-6))
+    assert abs(y[0, 0, 0] - 0.5) < 1e-6 and abs(z[0, 0, 0] - 2.0) < 1e-5
+
+
+@pytest.mark.parametrize("p", [2, 4])
+@pytest.mark.parametrize("tol,mi", [(0.0, 12), (1e-5, 100)])
+def test_cn_vs_oracle(golden, p, tol, mi):
+    a = golden["solvers"]["a"]
+    x, rep = roots.batched_coupled_newton(a, roots.CnConfig(p=p, tolerance=tol, max_iters=mi))
+    xo, ro = core.batched_coupled_newton(a, p, tol, mi)
+    for i in range(a.shape[0]):
+        assert relf(x[i], xo[i]) < 5e-5
+    assert all(abs(r.iterations - q.iterations) <= 1 for r, q in zip(rep, ro))
+
+
+@pytest.mark.parametrize("p", [2, 4])
+def test_clenshaw_vs_golden(golden, p):
+    g = golden["solvers"]
+    c = chebyshev.fit_inverse_root(p)
+    np.testing.assert_allclose(c.coeffs, g[f"cheb{p}_coeffs"], rtol=1e-12, atol=1e-14)
+    out = chebyshev.batched_clenshaw_matrix(g["a"], c, g[f"cheb{p}_scales"])
+    for i in range(out.shape[0]):
+        assert relf(out[i], g[f"cheb{p}_out"][i]) < 1e-3
+
+
+def test_ndb_fixed_iterations_large_block():
+    """B = 512 fixed 10-iteration chain vs the float64 oracle (fp32-class accumulation tolerance)."""
+    a = np.stack([core.random_spd(512, c, seed=10 + i, scale=0.5) for i, c in enumerate([10.0, 1e2])])
+    y, z, _ = roots.batched_newton_db(a, roots.NdbConfig(tolerance=0.0, max_iters=10))
+    yo, zo, _ = core.batched_newton_db(a, 0.0, 10)
+    assert relf(y[0], yo[0]) < 1e-4 and relf(z[1], zo[1]) < 5e-4
+
+
+def _run_step(case, shapes, b, method, golden, steps):
+    g = golden["steps"]
+    params = [g[f"{case}_param{i}"] for i in range(len(shapes))]
+    kw = solver_kwargs(method, spectral)
+    cfg = shampoo.ShampooConfig(block_size=b, solver=shampoo.SolverConfig(**kw),
+                                graft=shampoo.GraftConfig(beta1=0.9 if uses_momentum(method) else 0.0))
+    st = shampoo.init_state(params, cfg)
+    cur = [p.copy() for p in params]
+    for t in range(steps):
+        cur, st = shampoo.step(st, cur, [g[f"{case}_grad{t}_{i}"] for i in range(len(shapes))], cfg, seed=3)
+    return params, cur, st
+
+
+# Early-step statistics of the mini / ragged cases are rank deficient (1-3 EMA updates, cond ~1e10 with
+# eps = 1e-10 below fp32 resolution): fixed-iteration updates then agree to ~1e-3 (true fp32 shows the same,
+# SURVEY.md §7.3.3), and tolerance-mode solves are only meaningful on the full-rank "warm" case.
+# tolerance per (case kind, method): rank-deficient (mini, ragged) vs full-rank (warm)
+FIXED = {"ndbfix": (1.5e-3, 5e-4), "ndbfrofix": (1.5e-3, 5e-4), "cnfix4": (1.5e-3, 5e-4), "cbshv": (1e-2, 2e-3)}
+
+
+@pytest.mark.parametrize("case,shapes,b,nsteps,method,tol",
+                         [(c, s, b, n, m, t[c == "warm"]) for (c, s, b, n) in STEP_CASES for m, t in FIXED.items()]
+                         + [("warm", WARM, 16, 8, "ndbtol5", 2e-4), ("warm", WARM, 16, 8, "cntol5", 2e-4)])
+def test_step_vs_reference_golden(golden, case, shapes, b, nsteps, method, tol):
+    params, cur, st = _run_step(case, shapes, b, method, golden, nsteps)
+    g = golden["steps"]
+    for i, (p0, p1) in enumerate(zip(params, cur)):
+        want = g[f"{case}_{method}_out{i}"]
+        assert relf(p1 - p0, want - p0) < tol, f"layer {i}"
+    for gi, grp in enumerate(st.groups):
+        assert relf(grp.ema.cpu().numpy(), g[f"{case}_{method}_ema{gi}"]) < 2e-6
+
+
+def test_step_properties_zero_grad_and_update_norm():
+    """SPEC.md:571 zero grad -> params unchanged; SPEC.md:576 |delta theta|_F = eta |P|_F per block."""
+    rng = np.random.default_rng(0)
+    shapes = [(64, 96), (40,)]
+    params = [rng.standard_normal(s) for s in shapes]
+    cfg = shampoo.ShampooConfig(block_size=32, solver=shampoo.SolverConfig(tolerance=0.0, max_iters=10))
+    st = shampoo.init_state(params, cfg)
+    out, st = shampoo.step(st, params, [np.zeros(s) for s in shapes], cfg)
+    for p0, p1 in zip(params, out):  # theta is stored in fp32 on the device: unchanged up to that rounding
+        np.testing.assert_array_equal(p1, p0.astype(np.float32).astype(np.float64))
+    grads = [rng.standard_normal(s) for s in shapes]
+    st = shampoo.init_state(params, cfg)
+    out, st = shampoo.step(st, params, grads, cfg)
+    g = grads[0]
+    a_hat = (0.001 * g * g) / (1 - 0.999)
+    pdir = g / (1e-8 + np.sqrt(a_hat))
+    d = params[0] - out[0]
+    for (r0, r1), (c0, c1) in st.layers[0].layout.block_spans:
+        assert np.linalg.norm(d[r0:r1, c0:c1]) == pytest.approx(1e-3 * np.linalg.norm(pdir[r0:r1, c0:c1]), rel=1e-4)
+
+
+def test_c1_config_fixed_iterations_vs_oracle():
+    """Config 1: 1024x1024 layer, B=256, NDB (fixed 10 iterations/chain, PI scaling), one step."""
+    rng = np.random.default_rng(0)
+    w = rng.standard_normal((1024, 1024))
+    g = rng.standard_normal((1024, 1024))
+    cfg = shampoo.ShampooConfig(block_size=256, solver=shampoo.SolverConfig(method="ndb", tolerance=0.0, max_iters=10))
+    st = shampoo.init_state([w], cfg)
+    out, st = shampoo.step(st, [w], [g], cfg, seed=0)
+    ocfg = core.OracleConfig(block_size=256, method="ndb", tolerance=0.0, max_iters=10)
+    ost = core.init_state([w], ocfg)
+    oout, ost, _ = core.step(ost, [w], [g], ocfg, seed=0)
+    # literal C1 blocks have cond ~1e6 after one EMA step: fp32-class update error ~1e-2
+    assert relf(out[0] - w, oout[0] - w) < 2e-2
+    # the update norm identity holds per block regardless of conditioning
+    assert np.linalg.norm(out[0] - w) == pytest.approx(np.linalg.norm(oout[0] - w), rel=1e-4)
