@@ -50,6 +50,11 @@ typedef struct dash_plan dash_plan;
 /* Library / build identification. */
 const char* dash_version(void);
 int dash_device_sms(void);
+/* Instrumentation: number of kernels this library has launched (process lifetime), and optional
+ * CUDA-event timing of every tcgen05 GEMM launch on its own stream (algorithmic flops = 2 M N K per job). */
+unsigned long long dash_launch_count(void);
+void dash_gemm_timing(int enable);
+int dash_gemm_timing_read(int* launches, double* ms, double* flops);
 
 /* ---------------------------------------------------------------- dense primitives (linalg.py)
  * dash_split: fp32 stack (src[m*src_mat_stride + r*src_ld + c]) -> split-f16 stack.

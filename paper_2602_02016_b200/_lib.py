@@ -47,6 +47,10 @@ c_ull = ctypes.c_ulonglong
 _SIGNATURES: dict[str, tuple] = {
     "dash_version": (ctypes.c_char_p, []),
     "dash_device_sms": (c_int, []),
+    "dash_launch_count": (ctypes.c_ulonglong, []),
+    "dash_gemm_timing": (None, [c_int]),
+    "dash_gemm_timing_read": (c_int, [ctypes.POINTER(c_int), ctypes.POINTER(ctypes.c_double),
+                                      ctypes.POINTER(ctypes.c_double)]),
     "dash_split": (c_int, [c_void_p, c_longlong, c_int, _P, c_void_p]),
     "dash_unsplit": (c_int, [_P, c_void_p, c_longlong, c_int, c_void_p]),
     "dash_bmm_ws_bytes": (c_size_t, [c_int]),
@@ -121,3 +125,18 @@ def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
 def require_cuda(t: torch.Tensor, what: str) -> None:
     if not t.is_cuda:
         raise ValueError(f"{what} must be a CUDA tensor (the DASH B200 path has no CPU fallback)")
+
+
+def launch_count() -> int:
+    return int(lib().dash_launch_count())
+
+
+def gemm_timing(enable: bool) -> None:
+    lib().dash_gemm_timing(1 if enable else 0)
+
+
+def gemm_timing_read() -> tuple[int, float, float]:
+    """(launches, total ms, total algorithmic flops) of the GEMM launches since timing was enabled."""
+    n, ms, fl = ctypes.c_int(0), ctypes.c_double(0.0), ctypes.c_double(0.0)
+    check(lib().dash_gemm_timing_read(ctypes.byref(n), ctypes.byref(ms), ctypes.byref(fl)), "dash_gemm_timing_read")
+    return n.value, ms.value, fl.value

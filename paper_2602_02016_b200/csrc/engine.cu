@@ -121,14 +121,17 @@ int split_stack(const float* src, long long mat_stride, int src_ld, const dash_s
   cudaMemsetAsync(d.amax, 0, sizeof(unsigned) * d.nmat, st);
   amax_kernel<<<grid_for(static_cast<long long>(d.rows) * d.cols, d.nmat), 256, 0, st>>>(
       src, mat_stride, src_ld, d.rows, d.cols, d.amax);
+  note_launch();
   split_kernel<<<grid_for(static_cast<long long>(d.rows) * d.ld, d.nmat), 256, 0, st>>>(
       src, mat_stride, src_ld, d.rows, d.cols, reinterpret_cast<__half*>(d.data), d.ld, d.amax, d.exp);
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ECUDA;
 }
 
 int unsplit_stack(const dash_stack& s, float* dst, long long mat_stride, int dst_ld, cudaStream_t st) {
   unsplit_kernel<<<grid_for(static_cast<long long>(s.rows) * s.cols, s.nmat), 256, 0, st>>>(
       reinterpret_cast<const __half*>(s.data), s.rows, s.cols, s.ld, s.exp, dst, mat_stride, dst_ld);
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ECUDA;
 }
 
@@ -205,6 +208,8 @@ bool JobBuilder::upload(Arena& ar, cudaStream_t st, UploadedGemm* out) {
   out->jobs = reinterpret_cast<const GemmJob*>(d + mb);
   out->njobs = static_cast<int>(jobs.size());
   out->tiles = tiles;
+  out->flops = 0.0;
+  for (const GemmJob& j : jobs) out->flops += 2.0 * j.M * static_cast<double>(j.N) * j.K;
   return true;
 }
 
@@ -242,7 +247,9 @@ int JobBuilder::launch(void* ws, size_t ws_bytes, int passes, cudaStream_t st) {
   std::memcpy(staging.data() + maps.size() * sizeof(CUtensorMap), jobs.data(), jobs.size() * sizeof(GemmJob));
   if (cudaMemcpyAsync(base, staging.data(), staging.size(), cudaMemcpyHostToDevice, st) != cudaSuccess)
     return DASH_ECUDA;
-  return gemm_launch(d_jobs, static_cast<int>(jobs.size()), tiles, d_maps, passes, st);
+  double fl = 0.0;
+  for (const GemmJob& j : jobs) fl += 2.0 * j.M * static_cast<double>(j.N) * j.K;
+  return gemm_launch(d_jobs, static_cast<int>(jobs.size()), tiles, d_maps, passes, st, nullptr, fl);
 }
 
 }  // namespace dash
@@ -253,6 +260,13 @@ using namespace dash;
 extern "C" {
 
 const char* dash_version(void) { return "dash-b200 0.1 (sm_100a tcgen05)"; }
+
+unsigned long long dash_launch_count(void) { return g_launches; }
+void dash_gemm_timing(int enable) { gemm_timing_enable(enable); }
+int dash_gemm_timing_read(int* launches, double* ms, double* flops) {
+  if (!launches || !ms || !flops) return DASH_EINVAL;
+  return gemm_timing_read(launches, ms, flops);
+}
 
 int dash_device_sms(void) {
   int dev = 0, n = 0;

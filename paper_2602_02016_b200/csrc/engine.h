@@ -16,15 +16,20 @@ bool stack_ok(const dash_stack* s);
 int split_stack(const float* src, long long mat_stride, int src_ld, const dash_stack& d, cudaStream_t st);
 int unsplit_stack(const dash_stack& s, float* dst, long long mat_stride, int dst_ld, cudaStream_t st);
 int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtensorMap* d_maps, int passes,
-                cudaStream_t stream, const int* gate = nullptr);
+                cudaStream_t stream, const int* gate = nullptr, double flops = 0.0);
+void note_launch(int n = 1);  // count non-GEMM kernel launches
+extern unsigned long long g_launches;
+void gemm_timing_enable(int on);
+int gemm_timing_read(int* n, double* ms, double* flops);
 
 // A grouped GEMM whose maps + jobs already live in device memory.
 struct UploadedGemm {
   const GemmJob* jobs = nullptr;
   const CUtensorMap* maps = nullptr;
   int njobs = 0, tiles = 0;
+  double flops = 0.0;  // algorithmic: sum over jobs of 2 M N K
   int run(int passes, cudaStream_t st, const int* gate = nullptr) const {
-    return njobs ? gemm_launch(jobs, njobs, tiles, maps, passes, st, gate) : 0;
+    return njobs ? gemm_launch(jobs, njobs, tiles, maps, passes, st, gate, flops) : 0;
   }
 };
 

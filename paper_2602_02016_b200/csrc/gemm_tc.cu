@@ -11,6 +11,8 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <vector>
+
 #include "ptx.cuh"
 #include "types.h"
 
@@ -418,9 +420,37 @@ __global__ void __launch_bounds__(192, 1)
 // ---------------------------------------------------------------------------- host launcher
 static int g_num_sms = 0;
 
+// Launch accounting + optional CUDA-event timing of every GEMM launch (bench / roofline hooks).
+struct GemmTimer {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;  // start/stop pairs
+  std::vector<double> flops;
+  size_t used = 0;
+};
+static GemmTimer g_timer;
+unsigned long long g_launches = 0;
+
+void note_launch(int n) { g_launches += static_cast<unsigned long long>(n); }
+
 int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtensorMap* d_maps, int passes,
-                cudaStream_t stream, const int* gate) {
+                cudaStream_t stream, const int* gate, double flops) {
   if (total_tiles <= 0) return 0;
+  ++g_launches;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (g_timer.on) {
+    if (g_timer.used + 2 > g_timer.ev.size()) {
+      for (int i = 0; i < 256; ++i) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        g_timer.ev.push_back(e);
+      }
+    }
+    e0 = g_timer.ev[g_timer.used];
+    e1 = g_timer.ev[g_timer.used + 1];
+    g_timer.used += 2;
+    g_timer.flops.push_back(flops);
+    cudaEventRecord(e0, stream);
+  }
   if (g_num_sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -443,8 +473,32 @@ int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtenso
     }
     dash_gemm_kernel<1><<<grid, 192, GemmCfg<1>::kSmemBytes, stream>>>(d_jobs, njobs, total_tiles, d_maps, gate);
   }
+  if (e1) cudaEventRecord(e1, stream);
   err = cudaGetLastError();
   return err == cudaSuccess ? 0 : 3;
+}
+
+void gemm_timing_enable(int on) {
+  g_timer.on = on != 0;
+  g_timer.used = 0;
+  g_timer.flops.clear();
+}
+
+// Synchronises on the recorded events; returns launches timed, total ms and total algorithmic flops.
+int gemm_timing_read(int* n, double* ms, double* flops) {
+  double t = 0.0, f = 0.0;
+  const int k = static_cast<int>(g_timer.used / 2);
+  for (int i = 0; i < k; ++i) {
+    float x = 0.f;
+    if (cudaEventSynchronize(g_timer.ev[2 * i + 1]) != cudaSuccess) return 3;
+    cudaEventElapsedTime(&x, g_timer.ev[2 * i], g_timer.ev[2 * i + 1]);
+    t += x;
+    f += g_timer.flops[i];
+  }
+  *n = k;
+  *ms = t;
+  *flops = f;
+  return 0;
 }
 
 }  // namespace dash

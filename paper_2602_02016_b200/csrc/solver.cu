@@ -70,6 +70,7 @@ __global__ void zero_amax_gated_kernel(const int* gate, int n, unsigned* a, unsi
 
 static void zero_amax(const int* gate, int n, unsigned* a, unsigned* b, unsigned* c, cudaStream_t st) {
   zero_amax_gated_kernel<<<(n + 255) / 256, 256, 0, st>>>(gate, n, a, b, c);
+  note_launch();
 }
 
 // _DivergenceWatch.update (roots.py:77-86): keep 4 residuals, trip on 3 strict rises with >10x growth.
@@ -330,6 +331,7 @@ int scale_stack(const dash_stack& src, const float* mult, float pw, float* f_out
     cudaMemsetAsync(d.amax, 0, sizeof(unsigned) * d.nmat, st);
   }
   scale_stack_kernel<<<egrid(src), 256, 0, st>>>(src, mult, pw, f_out, f_mat_stride, f_ld, d, dst ? 1 : 0);
+  note_launch();
   return cuda_ok();
 }
 
@@ -350,6 +352,7 @@ __global__ void copy_if_kernel(const int* par, int want, dash_stack dst, dash_st
 
 static void copy_stack_if(const int* par, int want, const dash_stack& dst, const dash_stack& src, cudaStream_t st) {
   copy_if_kernel<<<1024, 256, 0, st>>>(par, want, dst, src);
+  note_launch();
 }
 
 // ---------------------------------------------------------------------------- NDB
@@ -421,16 +424,20 @@ int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_o
   }
   int np = 0;
   state_init_kernel<<<(n + 255) / 256, 256, 0, st>>>(s, n);
+  note_launch();
   // ---- iteration 1 (closed form): E1, Z1 = E1 into (e, z2); Y1 = a_hat E1 into y2
   cudaMemsetAsync(e.amax, 0, sizeof(unsigned) * n, st);
   cudaMemsetAsync(z2.amax, 0, sizeof(unsigned) * n, st);
   cudaMemsetAsync(y2.amax, 0, sizeof(unsigned) * n, st);
   ndb_first_kernel<<<egrid(a), 256, 0, st>>>(a, inv_scale, e, z2, s.resid);
+  note_launch();
   if (int rc = g_first.run(passes, st)) return rc;
   ++np;
   freeze_kernel<<<1, 1024, 0, st>>>(s, n, 1, tol, 1, iters, resid_out, conv, nullptr);
+  note_launch();
   set_par_kernel<<<1, 1, 0, st>>>(s.par, 1);  // Y1, Z1 live in the scratch pair
   int par = 1;
+  note_launch();
   for (int k = 2; k <= max_iters; ++k) {
     zero_amax(s.n_active, n, e.amax, nullptr, nullptr, st);
     if (int rc = g_e[par].run(passes, st, s.n_active)) return rc;
@@ -438,9 +445,11 @@ int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_o
     if (int rc = g_yz[par].run(passes, st, s.n_active)) return rc;
     np += 3;
     freeze_kernel<<<1, 1024, 0, st>>>(s, n, k, tol, 0, iters, resid_out, conv, nullptr);
+    note_launch();
     par ^= 1;
   }
   finish_kernel<<<(n + 255) / 256, 256, 0, st>>>(s, n, max_iters, iters, resid_out, conv);
+  note_launch();
   copy_stack_if(s.par, 1, y_out, y2, st);  // final iterate in the scratch pair -> outputs
   copy_stack_if(s.par, 1, z_out, z2, st);
   if (products) *products = np;
@@ -519,12 +528,14 @@ int cn_solve(const dash_stack& a, const float* inv_scale, int p, float c, const 
     if (!j2.upload(ar, st, &g_c4)) return DASH_EINVAL;
   }
   state_init_kernel<<<(n + 255) / 256, 256, 0, st>>>(s, n);
+  note_launch();
   cudaMemsetAsync(ms[0].amax, 0, sizeof(unsigned) * n, st);
   cudaMemsetAsync(corr.amax, 0, sizeof(unsigned) * n, st);
   cudaMemsetAsync(xs[0].amax, 0, sizeof(unsigned) * n, st);
   const float cpow_p = (p == 4) ? c * c * c * c : c * c;
   cn_first_kernel<<<egrid(a), 256, 0, st>>>(a, inv_scale, 1.f / c, 1.f / cpow_p, static_cast<float>(p), xs[0], ms[0],
                                             corr);
+  note_launch();
   int par = 0, np = 0;
   for (int k = 1; k <= max_iters; ++k) {
     zero_amax(s.n_active, n, xs[par ^ 1].amax, cp.amax, nullptr, st);
@@ -537,10 +548,13 @@ int cn_solve(const dash_stack& a, const float* inv_scale, int p, float c, const 
     if (int rc = g_m[par].run(passes, st, s.n_active)) return rc;
     np += (p == 4) ? 4 : 3;
     freeze_kernel<<<1, 1024, 0, st>>>(s, n, k, tol, 0, iters, resid_out, conv, newly);
+    note_launch();
     reset_identity_kernel<<<egrid(a), 256, 0, st>>>(corr, newly);
+    note_launch();
     par ^= 1;
   }
   finish_kernel<<<(n + 255) / 256, 256, 0, st>>>(s, n, max_iters, iters, resid_out, conv);
+  note_launch();
   copy_stack_if(s.par, 1, x_out, x2, st);
   if (products) *products = np;
   return cuda_ok();
@@ -682,8 +696,10 @@ int cheb_solve(const dash_stack& a, const float* inv_scale, const float* mult, c
   cudaMemsetAsync(sm.amax, 0, sizeof(unsigned) * n, st);
   cheb_first_kernel<<<egrid(a), 256, 0, st>>>(a, inv_scale, hc[degree], hc[degree - 1], sm, bb[(degree - 1) % 3],
                                               bb[degree % 3]);
+  note_launch();
   for (int k = degree - 2; k >= 1; --k) {
     pick_scalar_kernel<<<1, 1, 0, st>>>(cur, d_coef, k);
+    note_launch();
     cudaMemsetAsync(bb[k % 3].amax, 0, sizeof(unsigned) * n, st);
     if (int rc = g_rot[k % 3].run(passes, st)) return rc;
   }

@@ -546,10 +546,15 @@ int dash_plan_accumulate(dash_plan* p, float beta2, float beta1, int n_acc, floa
   cudaMemsetAsync(p->gamax, 0, sizeof(unsigned) * nb, st);
   prep_kernel<<<dim3(kPrepParts, nb), 256, 0, st>>>(p->dblocks, p->grad, p->adam, p->mom, beta2, beta1, bc1_inv,
                                                    bc2_inv, graft_eps, p->pn_part, p->gamax);
-  if (p->nb_m)
+  note_launch();
+  if (p->nb_m) {
     grad_split_kernel<<<dim3(32, p->nb_m), 256, 0, st>>>(p->dblocks, p->grad, p->gsm, p->gamax);
-  if (p->nb_v)
+    note_launch();
+  }
+  if (p->nb_v) {
     grad_split_kernel<<<dim3(4, p->nb_v), 256, 0, st>>>(p->dblocks + p->nb_m, p->grad, p->gsv, p->gamax + p->nb_m);
+    note_launch();
+  }
   if (int rc = p->g_stats.run(p->passes, st)) return rc;
   return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ECUDA;
 }
@@ -560,6 +565,7 @@ int dash_group_sym(float* ema, int n, int d, float eps, unsigned* amax, float* f
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaMemsetAsync(amax, 0, sizeof(unsigned) * n, st);
   sym_kernel<<<dim3(kPrepParts, n), 256, 0, st>>>(ema, d, eps, amax, fro_part);
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ECUDA;
 }
 
@@ -569,12 +575,14 @@ int dash_group_split_a(const float* ema, float eps, const dash_stack* a, void* s
   long long el = static_cast<long long>(a->rows) * a->ld;
   int gx = static_cast<int>(std::min<long long>(64, std::max<long long>(1, el / 4096)));
   a_split_kernel<<<dim3(gx, a->nmat), 256, 0, st>>>(ema, eps, *a);
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ECUDA;
 }
 
 int dash_fro_scale(const float* fro_part, int n, float* scale, float* inv_scale, void* stream) {
   if (!fro_part || n < 1 || !scale || !inv_scale) return DASH_EINVAL;
   fro_scale_kernel<<<(n + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(fro_part, n, scale, inv_scale);
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ECUDA;
 }
 
@@ -590,6 +598,7 @@ int dash_power_iteration(const float* ema, int n, int d, float eps, int pool, in
   }
   pi_kernel<<<n, kPiThreads, smem, static_cast<cudaStream_t>(stream)>>>(ema, d, eps, pool, iters, seed, scale,
                                                                         inv_scale, status);
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ECUDA;
 }
 
@@ -602,6 +611,7 @@ int dash_plan_apply(dash_plan* p, const float* theta_in, float* theta_out, float
   const int nb = p->nb_m + p->nb_v;
   update_kernel<<<dim3(16, nb), 256, 0, st>>>(p->dblocks, p->nb_m, p->bsz, p->pn_part, p->un_part, p->un_stride,
                                              p->um, p->uv, theta_in, theta_out, eta, p->graft_s);
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ECUDA;
 }
 
@@ -626,6 +636,7 @@ __global__ void uniform_kernel(unsigned long long seed, int count, double* out) 
 int dash_uniform_pm1(unsigned long long seed, int count, double* out, void* stream) {
   if (count < 0 || !out) return DASH_EINVAL;
   if (count) uniform_kernel<<<(count + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(seed, count, out);
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ECUDA;
 }
 

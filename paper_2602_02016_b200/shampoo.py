@@ -349,7 +349,7 @@ class _Runtime:
                 raise ValueError(f"layer {i}: shape {tuple(t.shape)} != {self.shapes[i]}")
             dst = flat[int(self.offsets[i]):int(self.offsets[i + 1])]
             if isinstance(t, torch.Tensor):
-                dst.copy_(t.reshape(-1), non_blocking=True)
+                dst.copy_(t.reshape(-1), non_blocking=t.is_cuda or t.is_pinned())
             else:
                 dst.copy_(torch.from_numpy(np.ascontiguousarray(t, dtype=np.float32).reshape(-1)))
 
@@ -485,28 +485,45 @@ def graft_scale(u, p) -> float:
     return float(np.linalg.norm(np.asarray(p.cpu() if isinstance(p, torch.Tensor) else p, dtype=np.float64))) / nu
 
 
-def step(state: ShampooState, params, grads, cfg: ShampooConfig, seed: int = 0, *, inplace: bool = False):
+def step(state: ShampooState, params, grads, cfg: ShampooConfig, seed: int = 0, *, inplace: bool = False,
+         events: dict | None = None):
     """One optimizer step; returns updated parameters and the mutated state (shampoo.py:362-404).
 
-    NumPy params -> new float64 NumPy arrays (like the reference).  CUDA tensors -> new fp32 tensors, or
-    the input tensors updated in place when ``inplace=True``.
+    NumPy params -> new float64 NumPy arrays (like the reference).  CPU tensors -> new fp32 CPU tensors
+    (pinned).  CUDA tensors -> new fp32 tensors, or the inputs updated in place when ``inplace=True``.
+    ``events`` (optional dict) collects CUDA events around the accumulate / refresh / apply phases.
     """
     if len(params) != len(state.layers):
         raise ValueError(f"expected {len(state.layers)} parameter tensors, got {len(params)}")
     rt: _Runtime = state.runtime
     t = state.step
+
+    def mark(name):
+        if events is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            events.setdefault(name, []).append(ev)
+
+    mark("start")
     accumulate(state, grads, cfg)
+    mark("accumulated")
     refresh_inverse_roots(state, cfg, seed=block_seed(seed, t))
+    mark("refreshed")
     eta = cfg.lr.value(t)
     rt.load(rt.theta, params)
     _lib.check(_lib.lib().dash_plan_apply(rt.plan, rt.theta.data_ptr(), rt.theta_out.data_ptr(), float(eta),
                                           _lib.stream_ptr()), "dash_plan_apply")
+    mark("applied")
     state.step = t + 1
-    outs = rt.views(rt.theta_out)
-    is_np = not isinstance(params[0], torch.Tensor)
-    if is_np:
+    if not isinstance(params[0], torch.Tensor):
         host = rt.theta_out.double().cpu().numpy()
         return [host[int(rt.offsets[i]):int(rt.offsets[i + 1])].reshape(s) for i, s in enumerate(rt.shapes)], state
+    if not params[0].is_cuda:
+        host = torch.empty(rt.theta_out.numel(), dtype=torch.float32, pin_memory=True)
+        host.copy_(rt.theta_out, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return [host[int(rt.offsets[i]):int(rt.offsets[i + 1])].view(s) for i, s in enumerate(rt.shapes)], state
+    outs = rt.views(rt.theta_out)
     if inplace:
         for p_, o in zip(params, outs):
             p_.copy_(o)
