@@ -126,12 +126,19 @@ int dash_plan_apply(dash_plan* p, const float* theta_in, float* theta_out, float
 /* Per-group refresh helpers (shampoo.py:312-349): symmetrize the EMA (linalg.symmetrize) and collect
  * max|a| / sum(a^2) partials of a = ema + eps I; split a; Frobenius scale; pooled power iteration
  * (spectral.py:87-117, block seeds block_seed(seed, i), NumPy-identical start vectors).
- * status[i]: 0 ok, 1 non-positive scale, 2 pool collapsed twice. */
+ * status[i]: 0 ok, 1 non-positive scale, 2 pool collapsed twice.  seed_index (device, nullable): global
+ * block index used for block i's child seed (block sharding keeps the 1-GPU pools). */
 int dash_group_sym(float* ema, int n, int d, float eps, uint32_t* amax, float* fro_part, void* stream);
 int dash_group_split_a(const float* ema, float eps, const dash_stack* a, void* stream);
 int dash_fro_scale(const float* fro_part, int n, float* scale, float* inv_scale, void* stream);
 int dash_power_iteration(const float* ema, int n, int d, float eps, int pool, int iters, unsigned long long seed,
-                         float* scale, float* inv_scale, int* status, void* stream);
+                         float* scale, float* inv_scale, int* status, const int* seed_index, void* stream);
+/* Block sharding exchange: copy blocks[b] (device table) of the flat space to/from the block-major
+ * packed buffer at offsets pos[b] (device), around the all-gather of updated parameter shards. */
+int dash_pack_blocks(const dash_block* blocks, int n, const long long* pos, const float* flat, float* packed,
+                     void* stream);
+int dash_unpack_blocks(const dash_block* blocks, int n, const long long* pos, const float* packed, float* flat,
+                       void* stream);
 /* spectral.block_seed (spectral.py:53-55), host side. */
 unsigned long long dash_block_seed(unsigned long long seed, unsigned long long index);
 /* First `count` draws of default_rng(seed).uniform(-1, 1), computed on the device (double). */

@@ -292,7 +292,8 @@ __device__ void pi_run(const float* a, int d, float eps, float* v, float* w, int
 __global__ void __launch_bounds__(kPiThreads, 1) pi_kernel(const float* __restrict__ ema, int d, float eps,
                                                            int pool, int iters, unsigned long long seed,
                                                            float* __restrict__ scale, float* __restrict__ inv_scale,
-                                                           int* __restrict__ status) {
+                                                           int* __restrict__ status,
+                                                           const int* __restrict__ seed_index) {
   extern __shared__ float pi_smem[];
   float* v = pi_smem;                  // d x 16
   float* w = v + d * kPiPool;          // d x 16
@@ -300,7 +301,9 @@ __global__ void __launch_bounds__(kPiThreads, 1) pi_kernel(const float* __restri
   __shared__ double nrm[kPiPool], q[kPiPool], vv[kPiPool], anrm;
   const int m = blockIdx.x;
   const float* a = ema + static_cast<long long>(m) * d * d;
-  uint64_t bseed = rng::block_seed(seed, static_cast<uint64_t>(m));
+  // block i of a group draws from block_seed(group_seed, i) (spectral.py:117); under block sharding the
+  // rank-local block m maps to its global index seed_index[m] so the pools are identical to 1 GPU.
+  uint64_t bseed = rng::block_seed(seed, static_cast<uint64_t>(seed_index ? seed_index[m] : m));
   float lam = 0.f;
   int st = 0;
   for (int attempt = 0; attempt < 2; ++attempt) {
@@ -372,6 +375,27 @@ __global__ void __launch_bounds__(256) update_kernel(const dash_block* __restric
     const int r = static_cast<int>(e / blk.cols), c = static_cast<int>(e % blk.cols);
     const long long i = blk.off + static_cast<long long>(r) * blk.ld + c;
     theta_out[i] = theta_in[i] - k * u[static_cast<long long>(r) * uld + c];
+  }
+}
+
+// ---------------------------------------------------------------------------- shard exchange
+// Block-major packing of (a subset of) the flat parameter space: block b occupies
+// packed[pos[b] .. pos[b] + rows*cols) in row-major order.  Used around the NCCL all-gather of the
+// updated parameter shards (one rank owns each gradient block).
+template <bool PACK>
+__global__ void __launch_bounds__(256) pack_kernel(const dash_block* __restrict__ blocks,
+                                                   const long long* __restrict__ pos, float* __restrict__ flat,
+                                                   float* __restrict__ packed) {
+  const int b = blockIdx.y;
+  const dash_block blk = blocks[b];
+  const long long total = static_cast<long long>(blk.rows) * blk.cols;
+  const long long base = pos[b];
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(e / blk.cols), c = static_cast<int>(e % blk.cols);
+    const long long i = blk.off + static_cast<long long>(r) * blk.ld + c;
+    if (PACK) packed[base + e] = flat[i];
+    else flat[i] = packed[base + e];
   }
 }
 
@@ -587,7 +611,7 @@ int dash_fro_scale(const float* fro_part, int n, float* scale, float* inv_scale,
 }
 
 int dash_power_iteration(const float* ema, int n, int d, float eps, int pool, int iters, unsigned long long seed,
-                         float* scale, float* inv_scale, int* status, void* stream) {
+                         float* scale, float* inv_scale, int* status, const int* seed_index, void* stream) {
   if (!ema || n < 1 || d < 1 || d > 1024 || pool < 1 || pool > kPiPool || iters < 1 || !scale || !inv_scale)
     return DASH_EINVAL;
   const size_t smem = static_cast<size_t>(d) * kPiPool * sizeof(float) * 2;
@@ -597,7 +621,7 @@ int dash_power_iteration(const float* ema, int n, int d, float eps, int pool, in
     attr = true;
   }
   pi_kernel<<<n, kPiThreads, smem, static_cast<cudaStream_t>(stream)>>>(ema, d, eps, pool, iters, seed, scale,
-                                                                        inv_scale, status);
+                                                                        inv_scale, status, seed_index);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ECUDA;
 }
@@ -617,6 +641,28 @@ int dash_plan_apply(dash_plan* p, const float* theta_in, float* theta_out, float
 
 int dash_plan_un_stride(const dash_plan* p) { return p ? p->un_stride : -1; }
 int dash_prep_parts(void) { return kPrepParts; }
+
+int dash_pack_blocks(const dash_block* blocks, int n, const long long* pos, const float* flat, float* packed,
+                     void* stream) {
+  if (n < 0 || (n && (!blocks || !pos || !flat || !packed))) return DASH_EINVAL;
+  if (n) {
+    pack_kernel<true><<<dim3(16, n), 256, 0, static_cast<cudaStream_t>(stream)>>>(blocks, pos, const_cast<float*>(flat),
+                                                                                 packed);
+    note_launch();
+  }
+  return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ECUDA;
+}
+
+int dash_unpack_blocks(const dash_block* blocks, int n, const long long* pos, const float* packed, float* flat,
+                       void* stream) {
+  if (n < 0 || (n && (!blocks || !pos || !flat || !packed))) return DASH_EINVAL;
+  if (n) {
+    pack_kernel<false><<<dim3(16, n), 256, 0, static_cast<cudaStream_t>(stream)>>>(blocks, pos, flat,
+                                                                                  const_cast<float*>(packed));
+    note_launch();
+  }
+  return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ECUDA;
+}
 
 unsigned long long dash_block_seed(unsigned long long seed, unsigned long long index) {
   return rng::block_seed(seed, index);

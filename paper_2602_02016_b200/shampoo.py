@@ -247,10 +247,36 @@ def init_state(params, cfg: ShampooConfig) -> ShampooState:
 
 
 # ============================================================================ device runtime
-class _Runtime:
-    """Flat device buffers + the C-ABI plan for one optimizer structure."""
+def block_rows(layers: list[LayerState], offsets, owned=None, slot_of=None):
+    """dash_block rows (off, ld, rows, cols, group_l, slot_l, group_r, slot_r): matrix blocks first.
 
-    def __init__(self, state: ShampooState, shapes, block_size: int, momentum: bool):
+    `owned`: optional set of (layer_id, block_idx) to keep (block sharding); `slot_of`: optional map
+    (layer_id, side, idx) -> SlotRef overriding the layer's refs (rank-local group numbering)."""
+    mats, vecs = [], []
+    for layer in layers:
+        base = int(offsets[layer.layer_id])
+        ref = (lambda side, i: slot_of[(layer.layer_id, side, i)]) if slot_of is not None else \
+            (lambda side, i: (layer.left_refs if side == "L" else layer.right_refs)[i])
+        if layer.is_matrix:
+            n = layer.shape[1]
+            for idx, ((r0, r1), (c0, c1)) in enumerate(layer.layout.block_spans):
+                if owned is not None and (layer.layer_id, idx) not in owned:
+                    continue
+                lr, rr = ref("L", idx), ref("R", idx)
+                mats.append((base + r0 * n + c0, n, r1 - r0, c1 - c0, lr.group, lr.slot, rr.group, rr.slot))
+        else:
+            for idx, (s, e) in enumerate(layer.chunk_bounds):
+                if owned is not None and (layer.layer_id, idx) not in owned:
+                    continue
+                lr = ref("L", idx)
+                vecs.append((base + s, 1, e - s, 1, lr.group, lr.slot, -1, -1))
+    return mats, vecs
+
+
+class _Runtime:
+    """Flat device buffers + the C-ABI plan for one optimizer structure (or one rank's shard of it)."""
+
+    def __init__(self, state: ShampooState, shapes, block_size: int, momentum: bool, owned=None, slot_of=None):
         self.dev = device()
         self.shapes = shapes
         self.bsz = block_size
@@ -263,19 +289,7 @@ class _Runtime:
         self.mom = torch.zeros(total, **f32) if momentum else None
         self.theta = torch.zeros(total, **f32)
         self.theta_out = torch.zeros(total, **f32)
-        # block table: matrix blocks (layer order, canonical block order) then 1-D chunks
-        mats, vecs = [], []
-        for layer in state.layers:
-            base = int(self.offsets[layer.layer_id])
-            if layer.is_matrix:
-                n = layer.shape[1]
-                for idx, ((r0, r1), (c0, c1)) in enumerate(layer.layout.block_spans):
-                    lr, rr = layer.left_refs[idx], layer.right_refs[idx]
-                    mats.append((base + r0 * n + c0, n, r1 - r0, c1 - c0, lr.group, lr.slot, rr.group, rr.slot))
-            else:
-                for idx, (s, e) in enumerate(layer.chunk_bounds):
-                    ref = layer.left_refs[idx]
-                    vecs.append((base + s, 1, e - s, 1, ref.group, ref.slot, -1, -1))
+        mats, vecs = block_rows(state.layers, self.offsets, owned, slot_of)
         self.nb_m, self.nb_v = len(mats), len(vecs)
         nb = self.nb_m + self.nb_v
         self.block_rows = mats + vecs
@@ -412,6 +426,9 @@ def refresh_inverse_roots(state: ShampooState, cfg: ShampooConfig, seed: int = 0
     rt: _Runtime = state.runtime
     solver = cfg.solver
     L = _lib.lib()
+    # block sharding: rank-local group gi is global group global_gid[gi]; its members' global slots
+    gids = getattr(rt, "global_gid", None)
+    sidx = getattr(rt, "seed_index", None)
     pending: list[tuple[PrecondGroup, list[DeviceReports]]] = []
     statuses = []
     for gi, group in enumerate(state.groups):
@@ -432,7 +449,8 @@ def refresh_inverse_roots(state: ShampooState, cfg: ShampooConfig, seed: int = 0
                                         _lib.stream_ptr()), "dash_fro_scale")
         else:
             power_iteration_scales(group.ema, cfg.epsilon, solver.scaling.pool, solver.scaling.iters,
-                                   block_seed(seed, gi), scale, inv, status)
+                                   block_seed(seed, gids[gi] if gids is not None else gi), scale, inv, status,
+                                   sidx[gi] if sidx is not None else None)
         statuses.append((group, scale, status))
         mode = solver.precision
         if solver.method == "cbshv":

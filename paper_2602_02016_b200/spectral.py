@@ -54,14 +54,17 @@ def block_seed(seed: int, index: int) -> int:
 
 
 def power_iteration_scales(ema: torch.Tensor, eps: float, pool: int, iters: int, seed: int,
-                           scale: torch.Tensor, inv_scale: torch.Tensor, status: torch.Tensor) -> None:
+                           scale: torch.Tensor, inv_scale: torch.Tensor, status: torch.Tensor,
+                           seed_index: torch.Tensor | None = None) -> None:
     """scale[i] = 2 * lambda_PI(ema[i] + eps I) with per-block seeds block_seed(seed, i) (device)."""
     if pool > MAX_POOL:
         raise ValueError(f"the B200 power iteration supports pool <= {MAX_POOL}")
     n, d = ema.shape[0], ema.shape[1]
     st = _lib.lib().dash_power_iteration(ema.data_ptr(), n, d, float(eps), int(pool), int(iters),
                                          int(seed) & (2**64 - 1), scale.data_ptr(), inv_scale.data_ptr(),
-                                         status.data_ptr(), _lib.stream_ptr())
+                                         status.data_ptr(),
+                                         seed_index.data_ptr() if seed_index is not None else None,
+                                         _lib.stream_ptr())
     _lib.check(st, "dash_power_iteration")
 
 
