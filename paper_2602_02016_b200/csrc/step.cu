@@ -13,9 +13,13 @@
 #include <cstring>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "engine.h"
 #include "ptx.cuh"
 #include "rng.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace dash {
 
@@ -345,6 +349,277 @@ __global__ void __launch_bounds__(kPiThreads, 1) pi_kernel(const float* __restri
   }
 }
 
+// ---------------------------------------------------------------------------- power iteration v2
+// A thread-block cluster of C CTAs per block (C = ceil(d / 128) <= 8) splits the rows of A; every CTA
+// streams its row slab of A once per iteration (the 4 MB block stays L2-resident across the 31 passes
+// because only ~18 blocks are in flight), keeps the full pool V (d x 16, fp32) in shared memory, and the
+// clusters exchange column norms and the new V rows through distributed shared memory.  A is symmetric,
+// so the slab A[rows, k-tile] is loaded as the contiguous k-major tile A[k-tile, rows].
+constexpr int kPi2Threads = 256;
+constexpr int kPi2KT = 32;     // k rows per A tile
+constexpr int kPi2R = 128;     // max rows per CTA
+
+struct Pi2Smem {
+  static size_t bytes(int d) {
+    return sizeof(float) * (2 * static_cast<size_t>(d) * kPiPool + 2 * kPi2KT * kPi2R + kPi2R * kPiPool +
+                            128 * kPiPool) +
+           sizeof(double) * (8 * kPiPool * 3 + 16 * kPiPool) + 64;
+  }
+};
+
+// A tile = rows k0..k0+KT of A restricted to columns row0..row0+R (== rows of A by symmetry); each of the
+// 256 threads owns KT*R/256 = 16 consecutive floats (4 float4 when the slab is 16-byte aligned).
+struct Pi2Regs {
+  float x[16];
+};
+
+__device__ __forceinline__ void pi2_tile_fetch(const float* __restrict__ a, int d, float eps, int k0, int row0, int nr,
+                                               bool vec, Pi2Regs& g) {
+  const int base = threadIdx.x * 16;  // 16 consecutive elements of the KT x R tile
+  const int kk = base / kPi2R, r0 = base % kPi2R;
+  const int k = k0 + kk;
+  if (vec && k < d && r0 + 16 <= nr) {
+    const float4* src = reinterpret_cast<const float4*>(a + static_cast<long long>(k) * d + row0 + r0);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float4 t = __ldg(src + i);
+      g.x[4 * i] = t.x; g.x[4 * i + 1] = t.y; g.x[4 * i + 2] = t.z; g.x[4 * i + 3] = t.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      g.x[i] = (k < d && r0 + i < nr) ? __ldg(a + static_cast<long long>(k) * d + row0 + r0 + i) : 0.f;
+  }
+  const int di = k - row0 - r0;  // diagonal element inside this thread's segment?
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+    if (i == di && k < d && r0 + i < nr) g.x[i] += eps;
+}
+
+__device__ __forceinline__ void pi2_tile_store(const Pi2Regs& g, float* __restrict__ dst) {
+  float4* d4 = reinterpret_cast<float4*>(dst + threadIdx.x * 16);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) d4[i] = make_float4(g.x[4 * i], g.x[4 * i + 1], g.x[4 * i + 2], g.x[4 * i + 3]);
+}
+
+// W[r][0..15] = sum_k A[row0 + r][k] V[k][0..15] for this CTA's rows (thread tile 4 rows x 4 cols, two
+// k-halves reduced through shared memory); the next A tile is fetched into registers while the current
+// one is consumed.
+__device__ void pi2_matvec(const float* __restrict__ a, int d, float eps, int row0, int nr, const float* __restrict__ v,
+                           float* __restrict__ tiles, float* __restrict__ w, float* __restrict__ red) {
+  const int t = threadIdx.x, half = t / 128, tt = t % 128, rg = tt / 4, cgi = tt % 4;
+  const bool vec = (d % 4 == 0) && (row0 % 4 == 0);
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  Pi2Regs g;
+  pi2_tile_fetch(a, d, eps, 0, row0, nr, vec, g);
+  pi2_tile_store(g, tiles);
+  __syncthreads();
+  int buf = 0;
+  for (int k0 = 0; k0 < d; k0 += kPi2KT) {
+    const bool more = k0 + kPi2KT < d;
+    if (more) pi2_tile_fetch(a, d, eps, k0 + kPi2KT, row0, nr, vec, g);
+    const float* tl = tiles + buf * kPi2KT * kPi2R;
+    const int kend = min(kPi2KT, d - k0);
+#pragma unroll 4
+    for (int kk = half; kk < kend; kk += 2) {
+      const float4 av = *reinterpret_cast<const float4*>(tl + kk * kPi2R + 4 * rg);
+      const float4 vv = *reinterpret_cast<const float4*>(v + (k0 + kk) * kPiPool + 4 * cgi);
+      const float ar[4] = {av.x, av.y, av.z, av.w};
+      const float vr[4] = {vv.x, vv.y, vv.z, vv.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(ar[i], vr[j], acc[i][j]);
+    }
+    if (more) pi2_tile_store(g, tiles + (buf ^ 1) * kPi2KT * kPi2R);
+    __syncthreads();
+    buf ^= 1;
+  }
+  if (half == 1) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) red[tt * 16 + i * 4 + j] = acc[i][j];
+  }
+  __syncthreads();
+  if (half == 0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = 4 * rg + i;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float x = acc[i][j] + red[tt * 16 + i * 4 + j];
+        if (r < nr) w[r * kPiPool + 4 * cgi + j] = x;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Cluster-wide fixed-order column sums: out[j] = sum over ranks q of (sum over my rows of f(x, y)).
+__device__ void pi2_colsum(cg::cluster_group& cl, int C, int q, const float* __restrict__ x, int xstride,
+                           const float* __restrict__ y, int nr, double* stripes, double* slots, double* out) {
+  const int t = threadIdx.x, j = t % kPiPool, s = t / kPiPool;  // 16 stripes
+  double acc = 0.0;
+  for (int r = s; r < nr; r += kPi2Threads / kPiPool) {
+    const double xv = x[r * xstride + j];
+    acc += xv * (y ? static_cast<double>(y[r * kPiPool + j]) : xv);
+  }
+  stripes[s * kPiPool + j] = acc;
+  __syncthreads();
+  if (t < kPiPool) {
+    double p = 0.0;
+    for (int i = 0; i < kPi2Threads / kPiPool; ++i) p += stripes[i * kPiPool + t];
+    for (int dst = 0; dst < C; ++dst) {
+      double* remote = cl.map_shared_rank(slots, dst);
+      remote[q * kPiPool + t] = p;
+    }
+  }
+  cl.sync();
+  if (t < kPiPool) {
+    double tot = 0.0;
+    for (int i = 0; i < C; ++i) tot += slots[i * kPiPool + t];
+    out[t] = tot;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kPi2Threads, 1) pi2_kernel(const float* __restrict__ ema, int d, float eps, int pool,
+                                                             int iters, unsigned long long seed,
+                                                             float* __restrict__ scale, float* __restrict__ inv_scale,
+                                                             int* __restrict__ status,
+                                                             const int* __restrict__ seed_index) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = static_cast<int>(cl.num_blocks());
+  const int q = static_cast<int>(cl.block_rank());
+  const int m = blockIdx.x / C;
+  const int R = (d + C - 1) / C;
+  const int row0 = q * R;
+  const int nr = max(0, min(R, d - row0));
+  extern __shared__ __align__(16) unsigned char pi2_raw[];
+  float* vbuf = reinterpret_cast<float*>(pi2_raw);                 // [2][d][16]
+  float* tiles = vbuf + 2 * d * kPiPool;                            // [2][KT][R]
+  float* w = tiles + 2 * kPi2KT * kPi2R;                            // [R][16]
+  float* red = w + kPi2R * kPiPool;                                 // [128][16]
+  double* stripes = reinterpret_cast<double*>(red + 128 * kPiPool);  // [16][16]
+  double* slots = stripes + 16 * kPiPool;                           // [8][16]
+  double* colv = slots + 8 * kPiPool;                               // [16]
+  double* qv = colv + kPiPool;                                      // [16]
+  double* vv = qv + kPiPool;                                        // [16]
+  const float* a = ema + static_cast<long long>(m) * d * d;
+  uint64_t bseed = rng::block_seed(seed, static_cast<uint64_t>(seed_index ? seed_index[m] : m));
+  float lam = 0.f;
+  int st = 0;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    // ---- start vectors for my rows: element (j, i) is draw j*d + i of default_rng(bseed)
+    float* v = vbuf;
+    const int per = (nr + 15) / 16;  // rows per (j, chunk) task
+    for (int task = threadIdx.x; task < kPiPool * 16; task += kPi2Threads) {
+      const int j = task / 16, c = task % 16;
+      const int r0 = c * per, r1 = min(nr, r0 + per);
+      if (r0 >= r1) continue;
+      if (j < pool) {
+        rng::Pcg64 g;
+        g.seed(bseed);
+        g.advance(static_cast<uint64_t>(j) * d + row0 + r0);
+        for (int r = r0; r < r1; ++r) w[r * kPiPool + j] = static_cast<float>(g.uniform_pm1());
+      } else {
+        for (int r = r0; r < r1; ++r) w[r * kPiPool + j] = 0.f;
+      }
+    }
+    __syncthreads();
+    pi2_colsum(cl, C, q, w, kPiPool, nullptr, nr, stripes, slots, colv);
+    // normalize (zero norm -> 1) and broadcast my rows of V0 to every CTA of the cluster
+    for (int i = threadIdx.x; i < nr * kPiPool; i += kPi2Threads) {
+      const int j = i % kPiPool;
+      double n = sqrt(colv[j]);
+      if (n == 0.0) n = 1.0;
+      const float x = static_cast<float>(w[i] / n);
+      for (int dst = 0; dst < C; ++dst) cl.map_shared_rank(v, dst)[row0 * kPiPool + i] = x;
+    }
+    cl.sync();
+    int cur = 0;
+    for (int it = 0; it < iters; ++it) {
+      const float* vc = vbuf + cur * d * kPiPool;
+      float* vn = vbuf + (cur ^ 1) * d * kPiPool;
+      pi2_matvec(a, d, eps, row0, nr, vc, tiles, w, red);
+      pi2_colsum(cl, C, q, w, kPiPool, nullptr, nr, stripes, slots, colv);
+      for (int i = threadIdx.x; i < nr * kPiPool; i += kPi2Threads) {
+        const double n = sqrt(colv[i % kPiPool]);
+        const float x = n > 0.0 ? static_cast<float>(w[i] / n) : 0.f;
+        for (int dst = 0; dst < C; ++dst) cl.map_shared_rank(vn, dst)[row0 * kPiPool + i] = x;
+      }
+      cl.sync();
+      cur ^= 1;
+    }
+    const float* vc = vbuf + cur * d * kPiPool;
+    pi2_matvec(a, d, eps, row0, nr, vc, tiles, w, red);  // A V once more for the quotients
+    pi2_colsum(cl, C, q, vc + row0 * kPiPool, kPiPool, w, nr, stripes, slots, qv);
+    pi2_colsum(cl, C, q, vc + row0 * kPiPool, kPiPool, nullptr, nr, stripes, slots, vv);
+    // every CTA evaluates the (identical) selection; rank 0 writes the result
+    int best = -1;
+    double bq = 0.0;
+    bool any = false;
+    for (int j = 0; j < pool; ++j) {
+      if (vv[j] > 0.0) {
+        if (!any || qv[j] > bq) { bq = qv[j]; best = j; }
+        any = true;
+      }
+    }
+    if (any && bq != 0.0) {
+      lam = static_cast<float>(bq / vv[best]);
+      break;
+    }
+    if (attempt == 0) {
+      bseed = rng::block_seed(bseed, 0x5EEDull);
+      st = 1;
+    } else {
+      st = 2;
+    }
+    cl.sync();
+  }
+  if (q == 0 && threadIdx.x == 0) {
+    const float s = 2.f * lam;
+    scale[m] = s;
+    inv_scale[m] = s > 0.f ? 1.f / s : 0.f;
+    if (status) status[m] = (st == 2) ? 2 : (s > 0.f ? 0 : 1);
+  }
+  cl.sync();  // keep every CTA's shared memory alive until all remote writes are done
+}
+
+static int pi2_launch(const float* ema, int n, int d, float eps, int pool, int iters, unsigned long long seed,
+                      float* scale, float* inv_scale, int* status, const int* seed_index, cudaStream_t st) {
+  int C = (d + kPi2R - 1) / kPi2R;
+  if (C > 8) return DASH_EINVAL;
+  if (C < 1) C = 1;
+  const size_t smem = Pi2Smem::bytes(d);
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(pi2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    attr = smem;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(n * C));
+  cfg.blockDim = dim3(kPi2Threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = C;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, pi2_kernel, ema, d, eps, pool, iters, seed, scale, inv_scale, status,
+                                     seed_index);
+  note_launch();
+  return e == cudaSuccess ? DASH_OK : DASH_ECUDA;
+}
+
 // ---------------------------------------------------------------------------- grafted update
 // theta_out = theta_in - eta * s_b * U with s_b = |P_b| / |U_b| (0 if |U_b| = 0) (shampoo.py:352-359, :393).
 __global__ void __launch_bounds__(256) update_kernel(const dash_block* __restrict__ blocks, int nb_m, int bsz,
@@ -614,6 +889,9 @@ int dash_power_iteration(const float* ema, int n, int d, float eps, int pool, in
                          float* scale, float* inv_scale, int* status, const int* seed_index, void* stream) {
   if (!ema || n < 1 || d < 1 || d > 1024 || pool < 1 || pool > kPiPool || iters < 1 || !scale || !inv_scale)
     return DASH_EINVAL;
+  if (d % 4 == 0 || d < 1024)  // cluster kernel (rows split over <= 8 CTAs)
+    return pi2_launch(ema, n, d, eps, pool, iters, seed, scale, inv_scale, status, seed_index,
+                      static_cast<cudaStream_t>(stream));
   const size_t smem = static_cast<size_t>(d) * kPiPool * sizeof(float) * 2;
   static bool attr = false;
   if (!attr) {
