@@ -159,8 +159,8 @@ bool JobBuilder::operands(GemmJob& j, const dash_stack& a, int am, int trans_a, 
   std::memset(&j, 0, sizeof(j));
   j.a_mn = trans_a ? 1 : 0;  // stored K x M -> MN-major
   j.b_mn = trans_b ? 0 : 1;  // stored K x N -> MN-major; stored N x K -> K-major
-  j.a_map = add_map(a, j.a_mn ? 64 : kTileM);
-  j.b_map = add_map(b, j.b_mn ? 64 : kTileN);
+  j.a_map = add_map(a, j.a_mn ? 64 : kTileM / 2);  // each CTA of the pair: 128 rows of A, 64 rows of B
+  j.b_map = add_map(b, 64);
   if (j.a_map < 0 || j.b_map < 0) return false;
   j.a_mat = am;
   j.b_mat = bm;
@@ -210,7 +210,18 @@ bool JobBuilder::upload(Arena& ar, cudaStream_t st, UploadedGemm* out) {
   out->tiles = tiles;
   out->flops = 0.0;
   for (const GemmJob& j : jobs) out->flops += 2.0 * j.M * static_cast<double>(j.N) * j.K;
+  out->uniform = uniform_tiles();
   return true;
+}
+
+int JobBuilder::uniform_tiles() const {
+  if (jobs.empty()) return 0;
+  const int t0 = jobs.size() > 1 ? jobs[1].tile_start - jobs[0].tile_start : tiles;
+  for (size_t i = 0; i < jobs.size(); ++i) {
+    const int next = i + 1 < jobs.size() ? jobs[i + 1].tile_start : tiles;
+    if (next - jobs[i].tile_start != t0 || jobs[i].tile_start != static_cast<int>(i) * t0) return 0;
+  }
+  return t0;
 }
 
 size_t stack_bytes(int nmat, int rows, int cols) {
@@ -249,7 +260,7 @@ int JobBuilder::launch(void* ws, size_t ws_bytes, int passes, cudaStream_t st) {
     return DASH_ECUDA;
   double fl = 0.0;
   for (const GemmJob& j : jobs) fl += 2.0 * j.M * static_cast<double>(j.N) * j.K;
-  return gemm_launch(d_jobs, static_cast<int>(jobs.size()), tiles, d_maps, passes, st, nullptr, fl);
+  return gemm_launch(d_jobs, static_cast<int>(jobs.size()), tiles, d_maps, passes, st, nullptr, fl, uniform_tiles());
 }
 
 }  // namespace dash

@@ -16,7 +16,7 @@ bool stack_ok(const dash_stack* s);
 int split_stack(const float* src, long long mat_stride, int src_ld, const dash_stack& d, cudaStream_t st);
 int unsplit_stack(const dash_stack& s, float* dst, long long mat_stride, int dst_ld, cudaStream_t st);
 int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtensorMap* d_maps, int passes,
-                cudaStream_t stream, const int* gate = nullptr, double flops = 0.0);
+                cudaStream_t stream, const int* gate = nullptr, double flops = 0.0, int uniform = 0);
 void note_launch(int n = 1);  // count non-GEMM kernel launches
 extern unsigned long long g_launches;
 void gemm_timing_enable(int on);
@@ -27,9 +27,10 @@ struct UploadedGemm {
   const GemmJob* jobs = nullptr;
   const CUtensorMap* maps = nullptr;
   int njobs = 0, tiles = 0;
+  int uniform = 0;     // tiles per job when all jobs have the same count (O(1) tile -> job), else 0
   double flops = 0.0;  // algorithmic: sum over jobs of 2 M N K
   int run(int passes, cudaStream_t st, const int* gate = nullptr) const {
-    return njobs ? gemm_launch(jobs, njobs, tiles, maps, passes, st, gate, flops) : 0;
+    return njobs ? gemm_launch(jobs, njobs, tiles, maps, passes, st, gate, flops, uniform) : 0;
   }
 };
 
@@ -80,6 +81,7 @@ struct JobBuilder {
   void push(GemmJob& j);
   static size_t bytes_for(int nmaps, int njobs);
   int launch(void* ws, size_t ws_bytes, int passes, cudaStream_t st);
+  int uniform_tiles() const;
   // Upload maps + jobs into the arena (one H2D copy); the builder may be reused afterwards.
   bool upload(Arena& ar, cudaStream_t st, UploadedGemm* out);
   size_t upload_bytes() const { return bytes_for(static_cast<int>(maps.size()), static_cast<int>(jobs.size())); }

@@ -634,7 +634,7 @@ __global__ void __launch_bounds__(256) update_kernel(const dash_block* __restric
   if (threadIdx.x == 0) {
     double pn = 0.0, un = 0.0;
     for (int p = 0; p < kPrepParts; ++p) pn += pn_part[b * kPrepParts + p];
-    const int ntiles = ((blk.rows + kTileM - 1) / kTileM) * ((blk.cols + kTileN - 1) / kTileN) * 4;
+    const int ntiles = ((blk.rows + kTileM - 1) / kTileM) * ((blk.cols + kTileN - 1) / kTileN) * kPartialsPerTile;
     for (int i = 0; i < ntiles; ++i) un += un_part[static_cast<long long>(b) * un_stride + i];
     const double s = un == 0.0 ? 0.0 : sqrt(pn) / sqrt(un);
     coef = static_cast<float>(static_cast<double>(eta) * s);
@@ -696,7 +696,9 @@ struct dash_plan {
 
 namespace dash {
 
-static int un_stride_for(int bsz) { return 4 * ((bsz + kTileM - 1) / kTileM) * ((bsz + kTileN - 1) / kTileN); }
+static int un_stride_for(int bsz) {
+  return kPartialsPerTile * ((bsz + kTileM - 1) / kTileM) * ((bsz + kTileN - 1) / kTileN);
+}
 
 static void set_dims(GemmJob& j, int M, int N, int K) {
   j.M = M;

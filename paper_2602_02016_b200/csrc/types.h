@@ -20,8 +20,9 @@ struct __half { unsigned short x; };
 
 namespace dash {
 
-constexpr int kTileM = 128;   // UMMA M (one CTA)
-constexpr int kTileN = 256;   // UMMA N
+constexpr int kTileM = 256;   // output tile rows (CTA pair, tcgen05 cta_group::2, 128 rows per CTA)
+constexpr int kTileN = 128;   // output tile columns (64 B rows staged per CTA)
+constexpr int kPartialsPerTile = 8;  // EPI_APPLY: 2 CTAs x 4 TMEM lane quarters
 constexpr int kTileK = 64;    // fp16 elements per 128-byte swizzle row
 constexpr int kLdAlign = 64;  // leading-dimension padding of split stacks (elements)
 constexpr int kEExp = -13;    // fixed exponent of identity-like Newton factors E (|E| < 8)
