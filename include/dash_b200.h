@@ -55,6 +55,9 @@ int dash_device_sms(void);
 unsigned long long dash_launch_count(void);
 void dash_gemm_timing(int enable);
 int dash_gemm_timing_read(int* launches, double* ms, double* flops);
+/* Per-launch detail of the timed GEMM launches: up to `cap` (ms, algorithmic flops, tiles) triples;
+ * returns the number written (or -status on error). */
+int dash_gemm_timing_list(int cap, double* ms, double* flops, int* tiles);
 
 /* ---------------------------------------------------------------- dense primitives (linalg.py)
  * dash_split: fp32 stack (src[m*src_mat_stride + r*src_ld + c]) -> split-f16 stack.
@@ -117,6 +120,8 @@ dash_plan* dash_plan_create(const dash_block* blocks, int nb_m, int nb_v, int bl
 void dash_plan_destroy(dash_plan* p);
 int dash_plan_un_stride(const dash_plan* p);
 int dash_prep_parts(void);
+/* Length of each block's slice of the apply-norm partial buffer (`un_part`) for a given block size. */
+int dash_apply_partials(int block_size);
 /* accumulate (shampoo.py:238-278): Adam / momentum EMA, block split of the gradient, L/R statistics EMA
  * as grouped tcgen05 GEMMs, and the per-block graft-direction norms |P_b|^2 for n_acc = t + 1. */
 int dash_plan_accumulate(dash_plan* p, float beta2, float beta1, int n_acc, float graft_eps, void* stream);

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -26,18 +27,19 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-bool make_stack_map(const dash_stack& s, int box_rows, CUtensorMap* out) {
+bool make_stack_map(const dash_stack& s, int box_rows, CUtensorMap* out, int box_cols, int box_planes, bool swz) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[4] = {static_cast<cuuint64_t>(s.ld), static_cast<cuuint64_t>(s.rows), 2,
                         static_cast<cuuint64_t>(s.nmat)};
   cuuint64_t strides[3] = {static_cast<cuuint64_t>(s.ld) * 2, static_cast<cuuint64_t>(s.rows) * s.ld * 2,
                            2ull * s.rows * s.ld * 2};
-  cuuint32_t box[4] = {static_cast<cuuint32_t>(kTileK), static_cast<cuuint32_t>(box_rows), 1, 1};
+  cuuint32_t box[4] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows),
+                       static_cast<cuuint32_t>(box_planes), 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, s.data, dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -136,15 +138,17 @@ int unsplit_stack(const dash_stack& s, float* dst, long long mat_stride, int dst
 }
 
 // ---------------------------------------------------------------------------- job assembly
-int JobBuilder::add_map(const dash_stack& s, int box_rows) {
-  for (size_t i = 0; i < map_keys.size(); ++i)
-    if (map_keys[i].data == s.data && map_keys[i].box == box_rows && map_keys[i].nmat == s.nmat &&
-        map_keys[i].rows == s.rows && map_keys[i].ld == s.ld)
+int JobBuilder::add_map(const dash_stack& s, int box_rows, int box_cols, int box_planes, bool swz) {
+  for (size_t i = 0; i < map_keys.size(); ++i) {
+    const MapKey& k = map_keys[i];
+    if (k.data == s.data && k.box == box_rows && k.box_cols == box_cols && k.planes == box_planes && k.swz == swz &&
+        k.nmat == s.nmat && k.rows == s.rows && k.ld == s.ld)
       return static_cast<int>(i);
+  }
   CUtensorMap m;
-  if (!make_stack_map(s, box_rows, &m)) return -1;
+  if (!make_stack_map(s, box_rows, &m, box_cols, box_planes, swz)) return -1;
   maps.push_back(m);
-  map_keys.push_back(MapKey{s.data, box_rows, s.nmat, s.rows, s.ld});
+  map_keys.push_back(MapKey{s.data, box_rows, s.nmat, s.rows, s.ld, box_cols, box_planes, swz});
   return static_cast<int>(maps.size()) - 1;
 }
 
@@ -173,6 +177,7 @@ bool JobBuilder::operands(GemmJob& j, const dash_stack& a, int am, int trans_a, 
   j.b_exp = b.exp + bm;
   j.b_amax = b.amax + bm;
   j.alpha = 1.f;
+  j.c_map = j.c_tmap = j.c2_map = j.c2_tmap = -1;
   return true;
 }
 
@@ -182,11 +187,41 @@ void JobBuilder::set_out(GemmJob& j, const dash_stack& c, int cm) {
   j.c_ld = c.ld;
   j.c_exp = c.exp + cm;
   j.c_amax = c.amax + cm;
+  j.c_rows = c.rows;
+  j.c_cols = c.cols;
+  j.c_mat = cm;
+  j.c_map = add_map(c, 32, 64, 2, true);
+  j.c_tmap = add_map(c, 64, 32, 2, false);
+}
+
+void JobBuilder::set_out2(GemmJob& j, const dash_stack& c, int cm) {
+  j.c2_hi = reinterpret_cast<__half*>(c.data) + static_cast<long long>(cm) * 2 * c.rows * c.ld;
+  j.c2_plane = static_cast<long long>(c.rows) * c.ld;
+  j.c2_exp = c.exp + cm;
+  j.c2_amax = c.amax + cm;
+  j.c2_mat = cm;
+  j.c2_map = add_map(c, 32, 64, 2, true);
+  j.c2_tmap = add_map(c, 64, 32, 2, false);
+}
+
+int job_tiles(const GemmJob& j) {
+  const int tm = (j.M + kTileM - 1) / kTileM;
+  if (!j.sym) return tm * j.tiles_n;
+  int n = 0;  // symmetric: column tiles J >= 2I of every 256-row tile I (see tile_coords)
+  for (int i = 0; i < tm; ++i) n += j.tiles_n - 2 * i;
+  return n;
 }
 
 void JobBuilder::push(GemmJob& j) {
+  static const int no_sym = getenv("DASH_NO_SYM") ? atoi(getenv("DASH_NO_SYM")) : 0;  // diagnostic knob
+  if (j.sym && (no_sym || j.M != j.N || j.op == EPI_EMA || j.op == EPI_APPLY)) j.sym = 0;
+  // TMA-staged split stores need the job to cover its output matrix exactly (padding stays zero)
+  static const int no_tma = getenv("DASH_NO_TMA_STORE") ? atoi(getenv("DASH_NO_TMA_STORE")) : 0;
+  if (no_tma || !j.c_hi || j.M != j.c_rows || j.N != j.c_cols || j.c_map < 0 || j.c_tmap < 0 ||
+      (j.c2_hi && (j.c2_map < 0 || j.c2_tmap < 0)))
+    j.c_map = j.c_tmap = j.c2_map = j.c2_tmap = -1;
   j.tile_start = tiles;
-  tiles += ((j.M + kTileM - 1) / kTileM) * j.tiles_n;
+  tiles += job_tiles(j);
   jobs.push_back(j);
 }
 
@@ -277,6 +312,11 @@ void dash_gemm_timing(int enable) { gemm_timing_enable(enable); }
 int dash_gemm_timing_read(int* launches, double* ms, double* flops) {
   if (!launches || !ms || !flops) return DASH_EINVAL;
   return gemm_timing_read(launches, ms, flops);
+}
+
+int dash_gemm_timing_list(int cap, double* ms, double* flops, int* tiles) {
+  if (cap < 0 || (cap > 0 && (!ms || !flops || !tiles))) return -DASH_EINVAL;
+  return gemm_timing_list(cap, ms, flops, tiles);
 }
 
 int dash_device_sms(void) {

@@ -11,8 +11,10 @@
 
 namespace dash {
 
-bool make_stack_map(const dash_stack& s, int box_rows, CUtensorMap* out);
+bool make_stack_map(const dash_stack& s, int box_rows, CUtensorMap* out, int box_cols = kTileK, int box_planes = 1,
+                    bool swz = true);
 bool stack_ok(const dash_stack* s);
+int job_tiles(const GemmJob& j);  // tiles the kernel runs for one job (fewer when j.sym)
 int split_stack(const float* src, long long mat_stride, int src_ld, const dash_stack& d, cudaStream_t st);
 int unsplit_stack(const dash_stack& s, float* dst, long long mat_stride, int dst_ld, cudaStream_t st);
 int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtensorMap* d_maps, int passes,
@@ -21,6 +23,7 @@ void note_launch(int n = 1);  // count non-GEMM kernel launches
 extern unsigned long long g_launches;
 void gemm_timing_enable(int on);
 int gemm_timing_read(int* n, double* ms, double* flops);
+int gemm_timing_list(int cap, double* ms, double* flops, int* tiles);
 
 // A grouped GEMM whose maps + jobs already live in device memory.
 struct UploadedGemm {
@@ -60,6 +63,8 @@ struct JobBuilder {
   struct MapKey {
     const void* data;
     int box, nmat, rows, ld;
+    int box_cols, planes;
+    bool swz;
   };
   std::vector<CUtensorMap> maps;
   std::vector<MapKey> map_keys;
@@ -73,11 +78,12 @@ struct JobBuilder {
     jobs.clear();
     tiles = 0;
   }
-  int add_map(const dash_stack& s, int box_rows);
+  int add_map(const dash_stack& s, int box_rows, int box_cols = kTileK, int box_planes = 1, bool swz = true);
   // check = false: the caller overrides M/N/K afterwards (sub-matrices of zero-padded slots)
   bool operands(GemmJob& j, const dash_stack& a, int am, int trans_a, const dash_stack& b, int bm, int trans_b,
                 bool check = true);
   void set_out(GemmJob& j, const dash_stack& c, int cm);
+  void set_out2(GemmJob& j, const dash_stack& c, int cm);  // second split output (EPI_CN_M correction)
   void push(GemmJob& j);
   static size_t bytes_for(int nmaps, int njobs);
   int launch(void* ws, size_t ws_bytes, int passes, cudaStream_t st);

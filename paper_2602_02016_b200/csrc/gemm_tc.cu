@@ -46,16 +46,17 @@ __device__ __forceinline__ void split_scaled(float y, __half& h, __half& l) {
   l = __float2half_rn(y - __half2float(h));
 }
 
-// Store 32 consecutive values of row r (cols c0..c0+31) as split fp16; masked variant for edges.
-__device__ __forceinline__ void store_split32(__half* hi, long long plane, int ld, int r, int c0, int M, int N,
-                                              const float (&x)[32], float inv_scale, bool& overflow) {
+// Store W (16 or 32) consecutive values of row r (cols c0..c0+W-1) as split fp16; masked variant for edges.
+template <int W>
+__device__ __forceinline__ void store_split(__half* hi, long long plane, int ld, int r, int c0, int M, int N,
+                                            const float (&x)[W], float inv_scale, bool& overflow) {
   if (r >= M) return;
   __half* ph = hi + static_cast<long long>(r) * ld + c0;
   __half* pl = ph + plane;
-  if (c0 + 32 <= N) {
-    uint32_t hw[16], lw[16];
+  if (c0 + W <= N) {
+    uint32_t hw[W / 2], lw[W / 2];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+    for (int i = 0; i < W / 2; ++i) {
       __half h0, l0, h1, l1;
       split_scaled(x[2 * i] * inv_scale, h0, l0);
       split_scaled(x[2 * i + 1] * inv_scale, h1, l1);
@@ -66,13 +67,13 @@ __device__ __forceinline__ void store_split32(__half* hi, long long plane, int l
     uint4* dh = reinterpret_cast<uint4*>(ph);
     uint4* dl = reinterpret_cast<uint4*>(pl);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < W / 8; ++i) {
       dh[i] = make_uint4(hw[4 * i], hw[4 * i + 1], hw[4 * i + 2], hw[4 * i + 3]);
       dl[i] = make_uint4(lw[4 * i], lw[4 * i + 1], lw[4 * i + 2], lw[4 * i + 3]);
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
+    for (int i = 0; i < W; ++i) {
       if (c0 + i < N) {
         __half h, l;
         split_scaled(x[i] * inv_scale, h, l);
@@ -84,48 +85,28 @@ __device__ __forceinline__ void store_split32(__half* hi, long long plane, int l
   }
 }
 
-__device__ __forceinline__ void load_split32(const __half* hi, long long plane, int ld, int r, int c0, int M,
-                                             int N, float scale, float (&x)[32]) {
-#pragma unroll
-  for (int i = 0; i < 32; ++i) x[i] = 0.f;
-  if (r >= M) return;
-  const __half* ph = hi + static_cast<long long>(r) * ld + c0;
-  const __half* pl = ph + plane;
-  if (c0 + 32 <= N) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      uint4 h = __ldg(reinterpret_cast<const uint4*>(ph) + i);
-      uint4 l = __ldg(reinterpret_cast<const uint4*>(pl) + i);
-      const __half2* h2 = reinterpret_cast<const __half2*>(&h);
-      const __half2* l2 = reinterpret_cast<const __half2*>(&l);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        float2 fh = __half22float2(h2[k]);
-        float2 fl = __half22float2(l2[k]);
-        x[8 * i + 2 * k] = (fh.x + fl.x) * scale;
-        x[8 * i + 2 * k + 1] = (fh.y + fl.y) * scale;
-      }
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < 32; ++i)
-      if (c0 + i < N) x[i] = (__half2float(ph[i]) + __half2float(pl[i])) * scale;
-  }
-}
-
-// ============================================================================ v2: CTA-pair kernel
+// ============================================================================ CTA-pair kernel
 // One thread-block cluster of 2 CTAs (a TPC pair) computes a 256 x 128 output tile with
 // tcgen05.mma.cta_group::2 (M = 256, N = 128, K = 16 per instruction): each CTA stages its 128 rows of A
 // and its 64 rows of B (N/2) per k-block; the leader CTA issues the MMAs; each CTA's TMEM receives its
-// 128 output rows.  tcgen05 accumulation truncates, so its error grows linearly with the number of
-// MMAs summed into one accumulator (profiles/r1_accumulation_error.log): k-block kb therefore goes to
-// accumulator kb % nacc of the tile (nacc x 128 TMEM columns) and the 4 epilogue warps sum the nacc
-// partials in fp32 registers (one row x 128 columns per thread).  nacc = 4 (split-f16 modes) cuts the
-// Newton-DB error 3.6x for ~9% time; nacc = 1 keeps 4 tiles in flight in TMEM.
+// 128 output rows.
+//
+// TMEM = 4 slots of 128 fp32 columns, each with its own full/empty barrier pair.  tcgen05 accumulation
+// truncates, so its error grows linearly with the number of MMAs summed into one accumulator
+// (profiles/r1_accumulation_error.log): a tile with nacc accumulators sends k-blocks
+// [c*per, (c+1)*per) to slot c (per = ceil(nk / nacc)) and the epilogue sums the partials in fp32.
+// Because each slot is committed as soon as its K range is done, the epilogue drains slot 0 while the
+// MMAs of slots 1..3 still run, and the next tile only waits for the slot it starts in -- the TMEM read
+// overlaps the tensor work instead of stalling it.  nacc = 1 (fp16 mode) keeps 4 tiles in flight.
+//
+// Symmetric jobs (jb.sym, C = C^T in exact arithmetic: every Newton / Chebyshev iterate is a polynomial
+// in the block) run only the tiles on or above the block diagonal; the epilogue stores each strictly-upper
+// 128 x 128 sub-block twice (direct and transposed) and drops the one below-diagonal sub-block of each
+// diagonal tile, so every output element has exactly one writer (deterministic).
 constexpr int kPairM = kTileM, kPairN = kTileN, kHalf = kTileM / 2, kHalfN = kTileN / 2;
-constexpr int kNaccDefault = 4;   // interleaved TMEM accumulators per tile, split-f16 (env DASH_NACC = 1, 2, 4)
-constexpr int kEpiWarps = 4;
-constexpr int kAccBufs = 4;       // TMEM accumulation buffers (4 x 128 columns = all 512)
+constexpr int kNaccDefault = 4;   // accumulators per tile in split-f16 modes (env DASH_NACC = 1, 2, 4)
+constexpr int kEpiWarps = 8;     // 2 per TMEM lane quarter, 64 columns each
+constexpr int kSlots = 4;         // TMEM accumulator slots (4 x 128 columns = all 512)
 constexpr int kThreads2 = 64 + 32 * kEpiWarps;
 
 template <int PASSES>
@@ -134,39 +115,91 @@ struct Gemm2Cfg {
   static constexpr int kABytes = kHalf * kTileK * 2;   // 16 KB per plane (128 rows of A)
   static constexpr int kBBytes = kHalfN * kTileK * 2;  // 8 KB per plane (64 rows of B)
   static constexpr int kStageBytes = (kABytes + kBBytes) * kPlanes;
-  static constexpr int kStages = PASSES == 3 ? 4 : 8;
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 512;
+  static constexpr int kStages = PASSES == 3 ? 3 : 6;
+  static constexpr int kEpiBytes = kEpiWarps * 8192;  // per epilogue warp: 32 x 64 split tile (2 planes)
+  static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 + 512;
 };
+
+// Tile `local` of a job -> (256-row tile ti, 128-column tile tj).  Symmetric jobs enumerate, per row tile
+// I, only the column tiles J >= 2I.
+__device__ __forceinline__ void tile_coords(const GemmJob& jb, int local, int& ti, int& tj) {
+  if (!jb.sym) {
+    ti = local / jb.tiles_n;
+    tj = local - ti * jb.tiles_n;
+    return;
+  }
+  int i = 0, row = jb.tiles_n;
+  while (local >= row) {
+    local -= row;
+    ++i;
+    row -= 2;
+  }
+  ti = i;
+  tj = 2 * i + local;
+}
+
+// Transposed store of 32 values of row r (cols c0..c0+31) into rows c0.. of column r (symmetric mirror).
+template <int W>
+__device__ __forceinline__ void store_split_T(__half* hi, long long plane, int ld, int r, int c0, int N,
+                                              const float (&x)[W], float inv_scale) {
+#pragma unroll
+  for (int i = 0; i < W; ++i) {
+    if (c0 + i < N) {
+      __half h, l;
+      split_scaled(x[i] * inv_scale, h, l);
+      __half* ph = hi + static_cast<long long>(c0 + i) * ld + r;
+      ph[0] = h;
+      ph[plane] = l;
+    }
+  }
+}
 
 struct EpiCtx {
   int op, mat, r, M, N;
-  bool inactive, row_ok;
+  bool inactive, row_ok, store, mirror;
   float sc, mul, gam, inv_out, inv_e, side_scale, cn_a, cn_b;
   float amax, amax2, resid;
   double sumsq;
   bool ovf, ovf2;
 };
 
-// Apply the fused DASH epilogue to 32 consecutive columns c0.. of row cx.r (x holds the fp32 product).
-__device__ __forceinline__ void epi_piece(const GemmJob& jb, EpiCtx& cx, int c0, float (&x)[32]) {
+template <int W>
+__device__ __forceinline__ void put_split(const EpiCtx& cx, __half* hi, long long plane, int ld, int c0,
+                                          const float (&x)[W], float inv, bool& ovf) {
+  if (!cx.store) return;
+  store_split<W>(hi, plane, ld, cx.r, c0, cx.M, cx.N, x, inv, ovf);
+  if (cx.mirror && cx.r < cx.M) store_split_T<W>(hi, plane, ld, cx.r, c0, cx.N, x, inv);
+}
+
+template <int W>
+__device__ __forceinline__ void put_f32(const EpiCtx& cx, float* f, int ld, int c0, const float (&x)[W]) {
+  if (!cx.store || cx.r >= cx.M) return;
+  float* fo = f + static_cast<long long>(cx.r) * ld + c0;
+#pragma unroll
+  for (int i = 0; i < W; ++i) if (c0 + i < cx.N) fo[i] = x[i];
+  if (cx.mirror) {
+#pragma unroll
+    for (int i = 0; i < W; ++i) if (c0 + i < cx.N) f[static_cast<long long>(c0 + i) * ld + cx.r] = x[i];
+  }
+}
+
+// Apply the fused DASH epilogue to W consecutive columns c0.. of row cx.r (x holds the fp32 product).
+template <int W>
+__device__ __forceinline__ void epi_piece(const GemmJob& jb, EpiCtx& cx, int c0, float (&x)[W], bool split_now) {
   const int r = cx.r;
   switch (cx.op) {
     case EPI_SPLIT: {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
+      for (int i = 0; i < W; ++i) {
         x[i] *= cx.sc * cx.mul;
         if (cx.row_ok && c0 + i < cx.N) cx.amax = nonneg_max(cx.amax, fabsf(x[i]));
       }
-      if (jb.c_hi) store_split32(jb.c_hi, jb.c_plane, jb.c_ld, r, c0, cx.M, cx.N, x, cx.inv_out, cx.ovf);
-      if (jb.f_out && cx.row_ok) {
-        float* fo = jb.f_out + static_cast<long long>(r) * jb.f_ld + c0;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) if (c0 + i < cx.N) fo[i] = x[i];
-      }
+      if (jb.c_hi && split_now) put_split<W>(cx, jb.c_hi, jb.c_plane, jb.c_ld, c0, x, cx.inv_out, cx.ovf);
+      if (jb.f_out) put_f32<W>(cx, jb.f_out, jb.f_ld, c0, x);
     } break;
     case EPI_NDB_E: {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
+      for (int i = 0; i < W; ++i) {
         const float d = (r == c0 + i) ? 1.f : 0.f;
         float e = 1.5f * d - 0.5f * (x[i] * cx.sc);
         if (cx.inactive) e = d;
@@ -176,23 +209,23 @@ __device__ __forceinline__ void epi_piece(const GemmJob& jb, EpiCtx& cx, int c0,
           cx.amax = nonneg_max(cx.amax, fabsf(e));
         }
       }
-      store_split32(jb.c_hi, jb.c_plane, jb.c_ld, r, c0, cx.M, cx.N, x, cx.inv_out, cx.ovf);
+      if (split_now) put_split<W>(cx, jb.c_hi, jb.c_plane, jb.c_ld, c0, x, cx.inv_out, cx.ovf);
     } break;
-    case EPI_EMA: {
+    case EPI_EMA: {  // never symmetric (host); fp32 read-modify-write
       if (cx.row_ok) {
         const float* fi = jb.f_in + static_cast<long long>(r) * jb.f_ld + c0;
         float* fo = jb.f_out + static_cast<long long>(r) * jb.f_ld + c0;
         const float b = jb.beta, omb = 1.f - jb.beta;
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
+        for (int i = 0; i < W; ++i)
           if (c0 + i < cx.N) fo[i] = b * fi[i] + omb * (x[i] * cx.sc);
       }
     } break;
-    case EPI_APPLY: {
+    case EPI_APPLY: {  // never symmetric (host)
       if (cx.row_ok) {
         float* fo = jb.f_out + static_cast<long long>(r) * jb.f_ld + c0;
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
+        for (int i = 0; i < W; ++i)
           if (c0 + i < cx.N) {
             const float u = x[i] * cx.sc;
             fo[i] = u;
@@ -206,7 +239,7 @@ __device__ __forceinline__ void epi_piece(const GemmJob& jb, EpiCtx& cx, int c0,
       const __half* sh = jb.s_hi + static_cast<long long>(r) * jb.s_ld + c0;
       const __half* sl = sh + jb.s_plane;
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
+      for (int i = 0; i < W; ++i) {
         float sv = 0.f;
         if (cx.row_ok && c0 + i < cx.N) sv = (__half2float(sh[i]) + __half2float(sl[i])) * cx.side_scale;
         const float d = (r == c0 + i) ? cx.gam : 0.f;
@@ -214,17 +247,13 @@ __device__ __forceinline__ void epi_piece(const GemmJob& jb, EpiCtx& cx, int c0,
         x[i] = y;
         if (cx.row_ok && c0 + i < cx.N) cx.amax = nonneg_max(cx.amax, fabsf(y));
       }
-      if (jb.c_hi) store_split32(jb.c_hi, jb.c_plane, jb.c_ld, r, c0, cx.M, cx.N, x, cx.inv_out, cx.ovf);
-      if (jb.f_out && cx.row_ok) {
-        float* fo = jb.f_out + static_cast<long long>(r) * jb.f_ld + c0;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) if (c0 + i < cx.N) fo[i] = x[i];
-      }
+      if (jb.c_hi && split_now) put_split<W>(cx, jb.c_hi, jb.c_plane, jb.c_ld, c0, x, cx.inv_out, cx.ovf);
+      if (jb.f_out) put_f32<W>(cx, jb.f_out, jb.f_ld, c0, x);
     } break;
     case EPI_CN_M: {
-      float cc[32];
+      float cc[W];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
+      for (int i = 0; i < W; ++i) {
         const float d = (r == c0 + i) ? 1.f : 0.f;
         const float m = x[i] * cx.sc;
         x[i] = m;
@@ -237,10 +266,60 @@ __device__ __forceinline__ void epi_piece(const GemmJob& jb, EpiCtx& cx, int c0,
           cx.amax2 = nonneg_max(cx.amax2, fabsf(c));
         }
       }
-      store_split32(jb.c_hi, jb.c_plane, jb.c_ld, r, c0, cx.M, cx.N, x, cx.inv_out, cx.ovf);
-      store_split32(jb.c2_hi, jb.c2_plane, jb.c_ld, r, c0, cx.M, cx.N, cc, cx.inv_e, cx.ovf2);
+      if (split_now) {
+        put_split<W>(cx, jb.c_hi, jb.c_plane, jb.c_ld, c0, x, cx.inv_out, cx.ovf);
+        put_split<W>(cx, jb.c2_hi, jb.c2_plane, jb.c_ld, c0, cc, cx.inv_e, cx.ovf2);
+      }
     } break;
     default: break;
+  }
+}
+
+// ---- SMEM-staged split stores (bulk tensor store per epilogue warp: 32 rows x 64 columns x 2 planes)
+// Direct layout: [plane][32 rows][128 B], 128-byte swizzle (16-byte chunk ch of row r at chunk ch ^ (r & 7)),
+// matching a {64, 32, 2, 1} tensor map with CU_TENSOR_MAP_SWIZZLE_128B.  f(v, col) gives the stored value.
+template <class F>
+__device__ __forceinline__ void stage_direct(uint8_t* buf, const float (&acc)[64], int lane, int c0, float inv,
+                                             F f, bool& ovf) {
+#pragma unroll
+  for (int ch = 0; ch < 8; ++ch) {
+    uint32_t hw[4], lw[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __half h0, l0, h1, l1;
+      split_scaled(f(acc[8 * ch + 2 * i], c0 + 8 * ch + 2 * i) * inv, h0, l0);
+      split_scaled(f(acc[8 * ch + 2 * i + 1], c0 + 8 * ch + 2 * i + 1) * inv, h1, l1);
+      ovf |= __hisinf(h0) | __hisinf(h1) | __hisnan(h0) | __hisnan(h1);
+      hw[i] = static_cast<uint32_t>(__half_as_ushort(h0)) | (static_cast<uint32_t>(__half_as_ushort(h1)) << 16);
+      lw[i] = static_cast<uint32_t>(__half_as_ushort(l0)) | (static_cast<uint32_t>(__half_as_ushort(l1)) << 16);
+    }
+    const int off = lane * 128 + ((ch ^ (lane & 7)) << 4);
+    *reinterpret_cast<uint4*>(buf + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+    *reinterpret_cast<uint4*>(buf + 4096 + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+  }
+}
+
+// Transposed layout: [plane][64 rows (= columns c0..c0+63)][32 columns (= this warp's rows) x 2 B], no swizzle,
+// matching a {32, 64, 2, 1} tensor map.  Built from the direct layout already in `buf` (after its bulk store
+// has read it): every lane reloads its own row, then writes it as a column -- one contiguous 64-byte row of
+// the transposed tile per column and warp.
+__device__ __forceinline__ void stage_transpose_in_place(uint8_t* buf, int lane) {
+  uint32_t hv[32], lv[32];
+#pragma unroll
+  for (int ch = 0; ch < 8; ++ch) {
+    const int off = lane * 128 + ((ch ^ (lane & 7)) << 4);
+    const uint4 h = *reinterpret_cast<const uint4*>(buf + off);
+    const uint4 l = *reinterpret_cast<const uint4*>(buf + 4096 + off);
+    hv[4 * ch] = h.x; hv[4 * ch + 1] = h.y; hv[4 * ch + 2] = h.z; hv[4 * ch + 3] = h.w;
+    lv[4 * ch] = l.x; lv[4 * ch + 1] = l.y; lv[4 * ch + 2] = l.z; lv[4 * ch + 3] = l.w;
+  }
+  __syncwarp();
+  uint16_t* bh = reinterpret_cast<uint16_t*>(buf) + lane;
+#pragma unroll
+  for (int j = 0; j < 64; ++j) {
+    const int sh = (j & 1) * 16;
+    bh[j * 32] = static_cast<uint16_t>(hv[j >> 1] >> sh);
+    bh[2048 + j * 32] = static_cast<uint16_t>(lv[j >> 1] >> sh);
   }
 }
 
@@ -249,17 +328,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     dash_gemm2_kernel(const GemmJob* __restrict__ jobs, int njobs, int total_tiles,
                       const CUtensorMap* __restrict__ maps, const int* __restrict__ gate, int nacc_in, int uniform) {
   using C = Gemm2Cfg<PASSES>;
-  const uint32_t nacc = static_cast<uint32_t>(nacc_in);      // accumulators per tile (1, 2 or 4)
-  const uint32_t nsets = kAccBufs / nacc;                     // tiles in flight in TMEM
+  const int nacc = nacc_in & 0xff;           // accumulators per tile (1, 2 or 4)
+  const int xp = nacc_in >> 8;               // experiment knobs (DASH_EXP): 1 = hi plane loads only, 2 = no stores
+  const uint32_t nsets = kSlots / nacc;      // tiles in flight in TMEM
 
   if (gate && *gate == 0) return;  // uniform across the grid (and thus across each pair)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes + C::kEpiBytes);
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
-  uint64_t* tempty = tfull + kAccBufs;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kAccBufs);
+  uint64_t* tempty = tfull + kSlots;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kSlots);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
@@ -271,13 +351,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       mbar_init(&full[s], 1);   // leader's arrive_expect_tx (both CTAs' TMA bytes land here)
       mbar_init(&empty[s], 1);  // pair-MMA commit (multicast to both CTAs)
     }
-    for (int a = 0; a < kAccBufs; ++a) {
+    for (int a = 0; a < kSlots; ++a) {
       mbar_init(&tfull[a], 1);                // pair-MMA commit (multicast)
       mbar_init(&tempty[a], 2 * kEpiWarps);   // every epilogue warp of both CTAs (leader's copy used)
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc2<kAccBufs * kPairN>(tmem_slot);
+  if (warp == 1) tmem_alloc2<kSlots * kPairN>(tmem_slot);
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
@@ -290,30 +370,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       uint32_t phase = 0;
       for (int tile = pair; tile < total_tiles; tile += npairs) {
         const GemmJob& jb = jobs[find_job(jobs, njobs, tile, uniform)];
-        const int local = tile - jb.tile_start;
-        const int am = (local / jb.tiles_n) * kPairM + kHalf * static_cast<int>(rank);
-        const int bn = (local % jb.tiles_n) * kPairN + kHalfN * static_cast<int>(rank);
+        int ti, tj;
+        tile_coords(jb, tile - jb.tile_start, ti, tj);
+        const int am = ti * kPairM + kHalf * static_cast<int>(rank);
+        const int bn = tj * kPairN + kHalfN * static_cast<int>(rank);
         const int nk = (jb.K + kTileK - 1) / kTileK;
         const CUtensorMap* amap = maps + jb.a_map;
         const CUtensorMap* bmap = maps + jb.b_map;
+        const int a_mn = jb.a_mn, b_mn = jb.b_mn, a_mat = jb.a_mat, b_mat = jb.b_mat;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * C::kStageBytes);
+          const int nplanes = (xp & 1) ? 1 : C::kPlanes;
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * C::kStageBytes / C::kPlanes * nplanes);
           uint8_t* sA = smem + stage * C::kStageBytes;
           uint8_t* sB = sA + C::kABytes * C::kPlanes;
           const int k0 = kb * kTileK;
 #pragma unroll
           for (int p = 0; p < C::kPlanes; ++p) {
+            if (p >= nplanes) break;
             uint8_t* a_dst = sA + p * C::kABytes;
             uint8_t* b_dst = sB + p * C::kBBytes;
-            if (!jb.a_mn) {
-              tma2_load_4d(a_dst, amap, &full[stage], k0, am, p, jb.a_mat);
+            if (!a_mn) {
+              tma2_load_4d(a_dst, amap, &full[stage], k0, am, p, a_mat);
             } else {
-              tma2_load_4d(a_dst, amap, &full[stage], am, k0, p, jb.a_mat);
-              tma2_load_4d(a_dst + 8192, amap, &full[stage], am + 64, k0, p, jb.a_mat);
+              tma2_load_4d(a_dst, amap, &full[stage], am, k0, p, a_mat);
+              tma2_load_4d(a_dst + 8192, amap, &full[stage], am + 64, k0, p, a_mat);
             }
-            if (!jb.b_mn) tma2_load_4d(b_dst, bmap, &full[stage], k0, bn, p, jb.b_mat);
-            else tma2_load_4d(b_dst, bmap, &full[stage], bn, k0, p, jb.b_mat);
+            if (!b_mn) tma2_load_4d(b_dst, bmap, &full[stage], k0, bn, p, b_mat);
+            else tma2_load_4d(b_dst, bmap, &full[stage], bn, k0, p, b_mat);
           }
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
@@ -321,8 +405,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer (leader CTA only)
-    // k-block kb of a tile accumulates into accumulator (kb % nacc) of the tile's buffer set; the
-    // accumulators are summed in fp32 by the epilogue, so each one holds only K / nacc of the sum.
     if (rank == 0 && elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
@@ -330,15 +412,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       for (int tile = pair; tile < total_tiles; tile += npairs, ++t) {
         const GemmJob& jb = jobs[find_job(jobs, njobs, tile, uniform)];
         const int nk = (jb.K + kTileK - 1) / kTileK;
+        const int per = (nk + nacc - 1) / nacc;  // k-blocks per accumulator slot
         const uint32_t idesc = umma_idesc_f16(kPairM, kPairN, jb.a_mn, jb.b_mn);
         const uint32_t a_lbo = jb.a_mn ? 8192u : 16u, b_lbo = jb.b_mn ? 8192u : 16u;
         const uint32_t a_kstep = jb.a_mn ? 2048u : 32u, b_kstep = jb.b_mn ? 2048u : 32u;
-        const uint32_t set = t % nsets;
-        mbar_wait(&tempty[set], ((t / nsets) & 1u) ^ 1u);
-        tc_fence_after();
+        const uint32_t base = (t % nsets) * static_cast<uint32_t>(nacc);
+        const uint32_t use_par = ((t / nsets) & 1u) ^ 1u;
+        int c = 0;
         for (int kb = 0; kb < nk; ++kb) {
-          const uint32_t d_tmem = tmem_base + (set * nacc + static_cast<uint32_t>(kb % nacc)) * kPairN;
-          const bool first = kb < nacc;
+          const bool first = (kb % per) == 0;
+          const uint32_t slot = base + static_cast<uint32_t>(c);
+          if (first) {
+            mbar_wait(&tempty[slot], use_par);
+            tc_fence_after();
+          }
+          const uint32_t d_tmem = tmem_base + slot * kPairN;
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_base = smem_u32(smem + stage * C::kStageBytes);
@@ -356,41 +444,57 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
           }
           umma2_commit_mc(&empty[stage]);
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+          if ((kb % per) == per - 1 || kb == nk - 1) {
+            umma2_commit_mc(&tfull[slot]);  // this slot's K range is complete
+            ++c;
+          }
         }
-        umma2_commit_mc(&tfull[set]);
+        for (; c < nacc; ++c) {  // slots without k-blocks (nk < nacc): keep every slot's phase in step
+          const uint32_t slot = base + static_cast<uint32_t>(c);
+          mbar_wait(&tempty[slot], use_par);
+          tc_fence_after();
+          umma2_commit_mc(&tfull[slot]);
+        }
       }
     }
   } else {
-    // ------------------------------------------------------------------ epilogue (warps 2..9, both CTAs)
-    const int q = warp & 3;  // TMEM lane quarter of this warp (warps 2..5 -> 2, 3, 0, 1)
-    const int half = 0;
+    // ------------------------------------------------------------------ epilogue (warps 2..9 of both CTAs)
+    const int q = warp & 3;                         // TMEM lane quarter (warps 2..9 -> 2, 3, 0, 1, 2, 3, 0, 1)
+    const int hc = static_cast<int>(warp - 2) >> 2;  // column half (64 columns) of this warp
+    uint8_t* ebuf = smem + C::kStages * C::kStageBytes + (warp - 2) * 8192;  // 1024-aligned staging tile
     const uint32_t leader_tempty = mapa_shared(smem_u32(tempty), 0);
     uint32_t t = 0;
     for (int tile = pair; tile < total_tiles; tile += npairs, ++t) {
       const GemmJob& jb = jobs[find_job(jobs, njobs, tile, uniform)];
       const int local = tile - jb.tile_start;
-      const int m0 = (local / jb.tiles_n) * kPairM;
-      const int n0 = (local % jb.tiles_n) * kPairN;
+      int ti, tj;
+      tile_coords(jb, local, ti, tj);
+      const int m0 = ti * kPairM;
+      const int n0 = tj * kPairN;
       const int nk = (jb.K + kTileK - 1) / kTileK;
-      const uint32_t set = t % nsets;
-      const int used = nk < static_cast<int>(nacc) ? nk : static_cast<int>(nacc);
-      float acc[128];
-      mbar_wait(&tfull[set], (t / nsets) & 1u);
-      tc_fence_after();
-      for (int c = 0; c < used; ++c) {
-        const uint32_t taddr =
-            tmem_base + (static_cast<uint32_t>(q * 32) << 16) + (set * nacc + static_cast<uint32_t>(c)) * kPairN;
+      const int per = (nk + nacc - 1) / nacc;
+      const int used = (nk + per - 1) / per;
+      const uint32_t base = (t % nsets) * static_cast<uint32_t>(nacc);
+      const uint32_t use_par = (t / nsets) & 1u;
+      float acc[64];
+      for (int c = 0; c < nacc; ++c) {
+        const uint32_t slot = base + static_cast<uint32_t>(c);
+        mbar_wait(&tfull[slot], use_par);
+        tc_fence_after();
+        if (c < used) {
+          const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + slot * kPairN + 64 * hc;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          float v[32];
-          tmem_ld32(taddr + 32 * j, v);
+          for (int j = 0; j < 2; ++j) {
+            float v[32];
+            tmem_ld32(taddr + 32 * j, v);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) acc[32 * j + i] = (c == 0) ? v[i] : acc[32 * j + i] + v[i];
+            for (int i = 0; i < 32; ++i) acc[32 * j + i] = (c == 0) ? v[i] : acc[32 * j + i] + v[i];
+          }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(leader_tempty + slot * 8);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_remote(leader_tempty + set * 8);
       // ---- fused epilogue on the fp32 sums
       EpiCtx cx;
       cx.op = jb.op;
@@ -398,7 +502,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       cx.r = m0 + kHalf * static_cast<int>(rank) + q * 32 + static_cast<int>(lane);
       cx.M = jb.M;
       cx.N = jb.N;
-      cx.row_ok = cx.r < jb.M;
+      // symmetric job: this CTA's 128 x 128 sub-block (row block 2 ti + rank, column block tj)
+      const int rb = 2 * ti + static_cast<int>(rank);
+      cx.store = !jb.sym || rb <= tj;
+      cx.mirror = jb.sym && rb < tj;
+      cx.row_ok = cx.r < jb.M && cx.store;
       const int ea = jb.a_exp ? __ldg(jb.a_exp) : 0;
       const int eb = jb.b_exp ? __ldg(jb.b_exp) : 0;
       cx.sc = ldexpf(1.f, ea + eb);
@@ -429,13 +537,68 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       cx.amax = cx.amax2 = cx.resid = 0.f;
       cx.sumsq = 0.0;
       cx.ovf = cx.ovf2 = false;
+      const bool tma_out = jb.c_map >= 0;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const int c0 = n0 + kHalf * half + 32 * j;
-        float v[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = acc[32 * j + i];
-        if (c0 < jb.N) epi_piece(jb, cx, c0, v);
+        const int c0 = n0 + 64 * hc + 16 * j;
+        float (&v)[16] = *reinterpret_cast<float(*)[16]>(&acc[16 * j]);  // in place: final values stay in acc
+        if (c0 < jb.N && !(xp & 2)) epi_piece<16>(jb, cx, c0, v, !tma_out);
+      }
+      if (tma_out && cx.store && !(xp & 2)) {
+        // ---- staged bulk-tensor stores of the split output(s), direct and (symmetric jobs) mirrored
+        const int r0 = m0 + kHalf * static_cast<int>(rank) + 32 * q;
+        const int c0 = n0 + 64 * hc;
+        const int lr = static_cast<int>(lane);
+        auto ident = [](float v, int) { return v; };
+        if (lane == 0) bulk_wait_read0();  // this warp's previous stores have read the buffer
+        __syncwarp();
+        stage_direct(ebuf, acc, lr, c0, cx.inv_out, ident, cx.ovf);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_4d(maps + jb.c_map, ebuf, c0, r0, 0, jb.c_mat);
+          bulk_commit();
+        }
+        if (cx.mirror) {
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
+          stage_transpose_in_place(ebuf, lr);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_4d(maps + jb.c_tmap, ebuf, r0, c0, 0, jb.c_mat);
+            bulk_commit();
+          }
+        }
+        if (jb.c2_map >= 0) {  // EPI_CN_M: next correction C = (1 + 1/p) I - M / p (I when frozen)
+          const int r = cx.r;
+          const float ca = cx.cn_a, cb = cx.cn_b;
+          const bool inact = cx.inactive;
+          auto corr = [r, ca, cb, inact](float m, int col) {
+            const float d = (r == col) ? 1.f : 0.f;
+            return inact ? d : ca * d - cb * m;
+          };
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
+          stage_direct(ebuf, acc, lr, c0, cx.inv_e, corr, cx.ovf2);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_4d(maps + jb.c2_map, ebuf, c0, r0, 0, jb.c2_mat);
+            bulk_commit();
+          }
+          if (cx.mirror) {
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+            stage_transpose_in_place(ebuf, lr);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_4d(maps + jb.c2_tmap, ebuf, r0, c0, 0, jb.c2_mat);
+              bulk_commit();
+            }
+          }
+        }
       }
       // per-matrix reductions (max is order independent -> deterministic)
       float am = cx.ovf ? __uint_as_float(0x7fc00000u) : cx.amax;
@@ -444,8 +607,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       am = warp_max_nonneg(am);
       am2 = warp_max_nonneg(am2);
       rs = warp_max_nonneg(rs);
-      (void)half;
-      if (lane == 0) {
+      if (lane == 0 && cx.store) {
         if (jb.c_amax) atomic_max_nonneg(jb.c_amax, am);
         if (jb.c2_amax) atomic_max_nonneg(jb.c2_amax, am2);
         if (jb.resid && !cx.inactive)
@@ -454,15 +616,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       }
       if (cx.op == EPI_APPLY) {
         const double sacc = warp_sum_d(cx.sumsq);
-        if (lane == 0) jb.partial[local * kPartialsPerTile + rank * 4 + q] = static_cast<float>(sacc);
+        if (lane == 0) jb.partial[local * kPartialsPerTile + rank * 8 + hc * 4 + q] = static_cast<float>(sacc);
       }
     }
+    if (lane == 0) bulk_wait0();  // bulk stores complete before the CTA retires
   }
   tc_fence_before();
   cluster_sync_all();  // no CTA of the pair may exit while its peer still uses its TMEM / barriers
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc2<kAccBufs * kPairN>(tmem_base);
+    tmem_dealloc2<kSlots * kPairN>(tmem_base);
   }
 }
 
@@ -470,12 +633,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
 static int g_num_sms = 0;
 static int g_nacc = 0;
 static int g_dbg = -1;
+static int g_exp = -1;
 
 // Launch accounting + optional CUDA-event timing of every GEMM launch (bench / roofline hooks).
 struct GemmTimer {
   bool on = false;
   std::vector<cudaEvent_t> ev;  // start/stop pairs
   std::vector<double> flops;
+  std::vector<int> tiles;
   size_t used = 0;
 };
 static GemmTimer g_timer;
@@ -500,11 +665,16 @@ int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtenso
     e1 = g_timer.ev[g_timer.used + 1];
     g_timer.used += 2;
     g_timer.flops.push_back(flops);
+    g_timer.tiles.push_back(total_tiles);
     cudaEventRecord(e0, stream);
   }
   if (g_dbg < 0) {
     const char* e = getenv("DASH_GEMM_DEBUG");
     g_dbg = e ? atoi(e) : 0;
+  }
+  if (g_exp < 0) {
+    const char* e = getenv("DASH_EXP");
+    g_exp = e ? atoi(e) : 0;
   }
   if (g_nacc == 0) {
     const char* e = getenv("DASH_NACC");
@@ -527,7 +697,7 @@ int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtenso
       attr = true;
     }
     dash_gemm2_kernel<3><<<grid2, kThreads2, Gemm2Cfg<3>::kSmemBytes, stream>>>(d_jobs, njobs, total_tiles, d_maps,
-                                                                                gate, g_nacc, uniform);
+                                                                                gate, g_nacc | (g_exp << 8), uniform);
   } else {
     static bool attr = false;
     if (!attr) {
@@ -535,7 +705,7 @@ int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtenso
       attr = true;
     }
     dash_gemm2_kernel<1><<<grid2, kThreads2, Gemm2Cfg<1>::kSmemBytes, stream>>>(d_jobs, njobs, total_tiles, d_maps,
-                                                                                gate, 1, uniform);
+                                                                                gate, 1 | (g_exp << 8), uniform);
   }
   if (e1) cudaEventRecord(e1, stream);
   err = cudaGetLastError();
@@ -546,6 +716,21 @@ void gemm_timing_enable(int on) {
   g_timer.on = on != 0;
   g_timer.used = 0;
   g_timer.flops.clear();
+  g_timer.tiles.clear();
+}
+
+int gemm_timing_list(int cap, double* ms, double* flops, int* tiles) {
+  const int k = static_cast<int>(g_timer.used / 2);
+  const int n = k < cap ? k : cap;
+  for (int i = 0; i < n; ++i) {
+    float x = 0.f;
+    if (cudaEventSynchronize(g_timer.ev[2 * i + 1]) != cudaSuccess) return -3;
+    cudaEventElapsedTime(&x, g_timer.ev[2 * i], g_timer.ev[2 * i + 1]);
+    ms[i] = x;
+    flops[i] = g_timer.flops[i];
+    tiles[i] = g_timer.tiles[i];
+  }
+  return n;
 }
 
 // Synchronises on the recorded events; returns launches timed, total ms and total algorithmic flops.

@@ -383,6 +383,7 @@ int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_o
       if (!jb.operands(j, a, m, 0, e, m, 0)) return DASH_EINVAL;
       j.op = EPI_SPLIT;
       j.out_mat = m;
+      j.sym = 1;
       j.alpha_p = inv_scale;
       jb.set_out(j, ys[1], m);
       jb.push(j);
@@ -400,6 +401,7 @@ int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_o
       if (!je.operands(j, zc, m, 0, yc, m, 0)) return DASH_EINVAL;
       j.op = EPI_NDB_E;
       j.out_mat = m;
+      j.sym = 1;
       j.active = s.active;
       j.resid = s.resid;
       je.set_out(j, e, m);
@@ -412,11 +414,13 @@ int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_o
       if (!jy.operands(j, yc, m, 0, e, m, 0)) return DASH_EINVAL;
       j.op = EPI_SPLIT;
       j.out_mat = m;
+      j.sym = 1;
       jy.set_out(j, yn, m);
       jy.push(j);
       if (!jy.operands(j, e, m, 0, zc, m, 0)) return DASH_EINVAL;
       j.op = EPI_SPLIT;
       j.out_mat = m;
+      j.sym = 1;
       jy.set_out(j, zn, m);
       jy.push(j);
     }
@@ -489,11 +493,11 @@ int cn_solve(const dash_stack& a, const float* inv_scale, int p, float c, const 
     for (int m = 0; m < n; ++m) {
       GemmJob j;
       if (!j1.operands(j, xs[par], m, 0, corr, m, 0)) return DASH_EINVAL;
-      j.op = EPI_SPLIT; j.out_mat = m;
+      j.op = EPI_SPLIT; j.out_mat = m; j.sym = 1;
       j1.set_out(j, xs[par ^ 1], m);
       j1.push(j);
       if (!j1.operands(j, corr, m, 0, corr, m, 0)) return DASH_EINVAL;
-      j.op = EPI_SPLIT; j.out_mat = m;
+      j.op = EPI_SPLIT; j.out_mat = m; j.sym = 1;
       j1.set_out(j, cp, m);
       j1.push(j);
     }
@@ -503,15 +507,12 @@ int cn_solve(const dash_stack& a, const float* inv_scale, int p, float c, const 
     for (int m = 0; m < n; ++m) {
       GemmJob j;
       if (!j3.operands(j, cpow, m, 0, ms[par], m, 0)) return DASH_EINVAL;
-      j.op = EPI_CN_M; j.out_mat = m;
+      j.op = EPI_CN_M; j.out_mat = m; j.sym = 1;
       j.beta = static_cast<float>(p);
       j.active = s.active;
       j.resid = s.resid;
       j3.set_out(j, ms[par ^ 1], m);
-      j.c2_hi = reinterpret_cast<__half*>(corr.data) + static_cast<long long>(m) * 2 * corr.rows * corr.ld;
-      j.c2_plane = static_cast<long long>(corr.rows) * corr.ld;
-      j.c2_exp = corr.exp + m;
-      j.c2_amax = corr.amax + m;
+      j3.set_out2(j, corr, m);
       j3.push(j);
     }
     if (!j3.upload(ar, st, &g_m[par])) return DASH_EINVAL;
@@ -521,7 +522,7 @@ int cn_solve(const dash_stack& a, const float* inv_scale, int p, float c, const 
     for (int m = 0; m < n; ++m) {
       GemmJob j;
       if (!j2.operands(j, cp, m, 0, cp, m, 0)) return DASH_EINVAL;
-      j.op = EPI_SPLIT; j.out_mat = m;
+      j.op = EPI_SPLIT; j.out_mat = m; j.sym = 1;
       j2.set_out(j, c4, m);
       j2.push(j);
     }
@@ -666,6 +667,7 @@ int cheb_solve(const dash_stack& a, const float* inv_scale, const float* mult, c
       if (!jb.operands(j, sm, m, 0, bb[(r + 1) % 3], m, 0)) return DASH_EINVAL;
       j.op = EPI_CHEB;
       j.out_mat = m;
+      j.sym = 1;
       j.gamma_p = cur;
       side_input(j, bb[(r + 2) % 3], m);
       jb.set_out(j, bb[r], m);
@@ -680,6 +682,7 @@ int cheb_solve(const dash_stack& a, const float* inv_scale, const float* mult, c
       if (!jb.operands(j, sm, m, 0, bb[1], m, 0)) return DASH_EINVAL;
       j.op = EPI_CHEB_FINAL;
       j.out_mat = m;
+      j.sym = 1;
       j.gamma = hc[0];
       j.alpha_p = mult;
       side_input(j, bb[2], m);

@@ -921,6 +921,7 @@ int dash_plan_apply(dash_plan* p, const float* theta_in, float* theta_out, float
 
 int dash_plan_un_stride(const dash_plan* p) { return p ? p->un_stride : -1; }
 int dash_prep_parts(void) { return kPrepParts; }
+int dash_apply_partials(int block_size) { return block_size > 0 ? un_stride_for(block_size) : -1; }
 
 int dash_pack_blocks(const dash_block* blocks, int n, const long long* pos, const float* flat, float* packed,
                      void* stream) {

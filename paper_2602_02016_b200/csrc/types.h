@@ -22,7 +22,7 @@ namespace dash {
 
 constexpr int kTileM = 256;   // output tile rows (CTA pair, tcgen05 cta_group::2, 128 rows per CTA)
 constexpr int kTileN = 128;   // output tile columns (64 B rows staged per CTA)
-constexpr int kPartialsPerTile = 8;  // EPI_APPLY: 2 CTAs x 4 TMEM lane quarters
+constexpr int kPartialsPerTile = 16;  // EPI_APPLY: 2 CTAs x 4 TMEM lane quarters x 2 column halves
 constexpr int kTileK = 64;    // fp16 elements per 128-byte swizzle row
 constexpr int kLdAlign = 64;  // leading-dimension padding of split stacks (elements)
 constexpr int kEExp = -13;    // fixed exponent of identity-like Newton factors E (|E| < 8)
@@ -53,9 +53,14 @@ struct GemmJob {
   int c_ld;        // split output leading dim
   int f_ld;        // fp32 output / input leading dim
   int s_ld;        // side split input leading dim
-  int pad0;
+  int sym;         // 1: C is symmetric (M == N): only tiles on/above the diagonal run, the epilogue mirrors
   const int* a_exp;  const unsigned* a_amax;   // exponent / amax of the A matrix
   const int* b_exp;  const unsigned* b_amax;
+  // ---- TMA store maps of the split outputs (-1: direct stores): c_map / c2_map box 64 x 32 x 2 planes
+  //      (128-byte swizzle), c_tmap / c2_tmap box 32 x 64 x 2 planes (transposed mirror of symmetric jobs)
+  int c_map, c_tmap, c2_map, c2_tmap;
+  int c_rows, c_cols;  // dims of the output stack (TMA stores only when the job covers it exactly)
+  int c_mat, c2_mat;   // matrix index of the outputs within their stacks (TMA coordinate)
   // ---- split output (hi plane; lo plane at +c_plane elements)
   __half* c_hi; long long c_plane; int* c_exp; unsigned* c_amax;
   // ---- second split output (EPI_CN_M correction factor)

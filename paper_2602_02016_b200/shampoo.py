@@ -303,7 +303,7 @@ class _Runtime:
         L = _lib.lib()
         self.prep_parts = L.dash_prep_parts()
         self.pn_part = torch.zeros(nb * self.prep_parts, **f32)
-        self.un_stride = 8 * (-(-block_size // 256)) * (-(-block_size // 128))  # kPartialsPerTile x tiles
+        self.un_stride = L.dash_apply_partials(block_size)  # partials per tile x tiles of a full block
         self.un_part = torch.zeros(nb * self.un_stride, **f32)
         self.gamax = torch.zeros(nb, dtype=torch.int32, device=self.dev)
         self.graft_s = torch.zeros(nb, **f32)
