@@ -354,108 +354,124 @@ __global__ void __launch_bounds__(kPiThreads, 1) pi_kernel(const float* __restri
 // streams its row slab of A once per iteration (the 4 MB block stays L2-resident across the 31 passes
 // because only ~18 blocks are in flight), keeps the full pool V (d x 16, fp32) in shared memory, and the
 // clusters exchange column norms and the new V rows through distributed shared memory.  A is symmetric,
-// so the slab A[rows, k-tile] is loaded as the contiguous k-major tile A[k-tile, rows].
+// so the slab A[rows, k] is read as the contiguous row segment A[k, rows].
+//
+// Matvec thread tile: 4 rows x all 16 pool columns, 8 interleaved k-splits (one per warp: k = w, w + 8, ...).
+// Each k costs one coalesced 16-byte global load of A per thread (512 B per warp) and four broadcast
+// shared loads of V[k] for 64 FMAs, so the loop is FMA-bound instead of shared-memory bound; the eight
+// k-split partials are summed in a fixed order (deterministic, batch-independent).
 constexpr int kPi2Threads = 256;
-constexpr int kPi2KT = 32;     // k rows per A tile
-constexpr int kPi2R = 128;     // max rows per CTA
+constexpr int kPi2Cols = 16;      // pool columns per thread
+constexpr int kPi2R = 128;       // max rows per CTA (32 row groups of 4)
+constexpr int kPi2Splits = 8;     // interleaved k splits (one per warp)
+constexpr int kPi2Ahead = 4;     // k steps of A prefetched into registers
 
 struct Pi2Smem {
   static size_t bytes(int d) {
-    return sizeof(float) * (2 * static_cast<size_t>(d) * kPiPool + 2 * kPi2KT * kPi2R + kPi2R * kPiPool +
-                            128 * kPiPool) +
-           sizeof(double) * (8 * kPiPool * 3 + 16 * kPiPool) + 64;
+    return sizeof(float) * (2 * static_cast<size_t>(d) * kPiPool + static_cast<size_t>(kPi2Splits) * kPi2R * kPiPool +
+                            kPi2R * kPiPool) +
+           sizeof(double) * (8 * kPiPool * 3 + kPi2Threads) + 64;
   }
 };
 
-// A tile = rows k0..k0+KT of A restricted to columns row0..row0+R (== rows of A by symmetry); each of the
-// 256 threads owns KT*R/256 = 16 consecutive floats (4 float4 when the slab is 16-byte aligned).
-struct Pi2Regs {
-  float x[16];
-};
-
-__device__ __forceinline__ void pi2_tile_fetch(const float* __restrict__ a, int d, float eps, int k0, int row0, int nr,
-                                               bool vec, Pi2Regs& g) {
-  const int base = threadIdx.x * 16;  // 16 consecutive elements of the KT x R tile
-  const int kk = base / kPi2R, r0 = base % kPi2R;
-  const int k = k0 + kk;
-  if (vec && k < d && r0 + 16 <= nr) {
-    const float4* src = reinterpret_cast<const float4*>(a + static_cast<long long>(k) * d + row0 + r0);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float4 t = __ldg(src + i);
-      g.x[4 * i] = t.x; g.x[4 * i + 1] = t.y; g.x[4 * i + 2] = t.z; g.x[4 * i + 3] = t.w;
-    }
+// A[k, row0 + r4 .. + 3] (== A[rows, k] by symmetry); k is clamped into range and out-of-range steps are
+// zeroed by a select, so the unrolled k loop has no branches.  VEC: d, row0 and nr are multiples of 4.
+template <bool VEC>
+__device__ __forceinline__ float4 pi2_load_a(const float* __restrict__ a, int d, int k, int row0, int r4, int nr) {
+  const int kc = k < d ? k : d - 1;
+  const float* src = a + static_cast<long long>(kc) * d + row0;
+  float4 x;
+  if (VEC) {
+    x = __ldg(reinterpret_cast<const float4*>(src + (r4 < nr ? r4 : 0)));
+    if (r4 >= nr) x = make_float4(0.f, 0.f, 0.f, 0.f);
   } else {
-#pragma unroll
-    for (int i = 0; i < 16; ++i)
-      g.x[i] = (k < d && r0 + i < nr) ? __ldg(a + static_cast<long long>(k) * d + row0 + r0 + i) : 0.f;
+    x.x = r4 < nr ? __ldg(src + r4) : 0.f;
+    x.y = r4 + 1 < nr ? __ldg(src + r4 + 1) : 0.f;
+    x.z = r4 + 2 < nr ? __ldg(src + r4 + 2) : 0.f;
+    x.w = r4 + 3 < nr ? __ldg(src + r4 + 3) : 0.f;
   }
-  const int di = k - row0 - r0;  // diagonal element inside this thread's segment?
-#pragma unroll
-  for (int i = 0; i < 16; ++i)
-    if (i == di && k < d && r0 + i < nr) g.x[i] += eps;
+  if (k >= d) x = make_float4(0.f, 0.f, 0.f, 0.f);
+  return x;
 }
 
-__device__ __forceinline__ void pi2_tile_store(const Pi2Regs& g, float* __restrict__ dst) {
-  float4* d4 = reinterpret_cast<float4*>(dst + threadIdx.x * 16);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) d4[i] = make_float4(g.x[4 * i], g.x[4 * i + 1], g.x[4 * i + 2], g.x[4 * i + 3]);
-}
-
-// W[r][0..15] = sum_k A[row0 + r][k] V[k][0..15] for this CTA's rows (thread tile 4 rows x 4 cols, two
-// k-halves reduced through shared memory); the next A tile is fetched into registers while the current
-// one is consumed.
+// W[r][0..15] = sum_k (A + eps I)[row0 + r][k] V[k][0..15] for this CTA's rows; the eps I term is added
+// as eps V[row0 + r] in the fixed-order reduction.
+template <bool VEC>
 __device__ void pi2_matvec(const float* __restrict__ a, int d, float eps, int row0, int nr, const float* __restrict__ v,
-                           float* __restrict__ tiles, float* __restrict__ w, float* __restrict__ red) {
-  const int t = threadIdx.x, half = t / 128, tt = t % 128, rg = tt / 4, cgi = tt % 4;
-  const bool vec = (d % 4 == 0) && (row0 % 4 == 0);
-  float acc[4][4];
+                           float* __restrict__ red, float* __restrict__ w) {
+  const int t = threadIdx.x, rg = t & 31, ks = (t >> 5) % kPi2Splits, ch = (t >> 5) / kPi2Splits, r4 = 4 * rg;
+  float acc[4][kPi2Cols];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-  Pi2Regs g;
-  pi2_tile_fetch(a, d, eps, 0, row0, nr, vec, g);
-  pi2_tile_store(g, tiles);
-  __syncthreads();
-  int buf = 0;
-  for (int k0 = 0; k0 < d; k0 += kPi2KT) {
-    const bool more = k0 + kPi2KT < d;
-    if (more) pi2_tile_fetch(a, d, eps, k0 + kPi2KT, row0, nr, vec, g);
-    const float* tl = tiles + buf * kPi2KT * kPi2R;
-    const int kend = min(kPi2KT, d - k0);
-#pragma unroll 4
-    for (int kk = half; kk < kend; kk += 2) {
-      const float4 av = *reinterpret_cast<const float4*>(tl + kk * kPi2R + 4 * rg);
-      const float4 vv = *reinterpret_cast<const float4*>(v + (k0 + kk) * kPiPool + 4 * cgi);
-      const float ar[4] = {av.x, av.y, av.z, av.w};
-      const float vr[4] = {vv.x, vv.y, vv.z, vv.w};
+    for (int j = 0; j < kPi2Cols; ++j) acc[i][j] = 0.f;
+  if (VEC && d % (kPi2Splits * kPi2Ahead) == 0 && nr == kPi2R) {
+    // fast path (every DASH block size): no tail, full slab -> pointer-stepped loads, no selects
+    const long long st4 = static_cast<long long>(kPi2Splits) * d / 4;  // float4 stride between my k steps
+    const float4* p = reinterpret_cast<const float4*>(a + static_cast<long long>(ks) * d + row0 + r4);
+    const float4* vks = reinterpret_cast<const float4*>(v) + ks * (kPiPool / 4) + ch * (kPi2Cols / 4);
+    float4 pre[kPi2Ahead];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+    for (int u = 0; u < kPi2Ahead; ++u) pre[u] = __ldg(p + u * st4);
+    const int rounds = d / (kPi2Splits * kPi2Ahead);
+    for (int rd = 0; rd < rounds; ++rd) {
+      const bool more = rd + 1 < rounds;
+      const float4* pn = p + static_cast<long long>(kPi2Ahead) * (rd + 1) * st4;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(ar[i], vr[j], acc[i][j]);
-    }
-    if (more) pi2_tile_store(g, tiles + (buf ^ 1) * kPi2KT * kPi2R);
-    __syncthreads();
-    buf ^= 1;
-  }
-  if (half == 1) {
+      for (int u = 0; u < kPi2Ahead; ++u) {
+        const float4 av = pre[u];
+        if (more) pre[u] = __ldg(pn + u * st4);
+        const float4* vk = vks + (kPi2Ahead * rd + u) * kPi2Splits * (kPiPool / 4);
+        const float ar[4] = {av.x, av.y, av.z, av.w};
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+        for (int j4 = 0; j4 < kPi2Cols / 4; ++j4) {
+          const float4 vv = vk[j4];
+          const float vr[4] = {vv.x, vv.y, vv.z, vv.w};
 #pragma unroll
-      for (int j = 0; j < 4; ++j) red[tt * 16 + i * 4 + j] = acc[i][j];
-  }
-  __syncthreads();
-  if (half == 0) {
+          for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int r = 4 * rg + i;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float x = acc[i][j] + red[tt * 16 + i * 4 + j];
-        if (r < nr) w[r * kPiPool + 4 * cgi + j] = x;
+            for (int j = 0; j < 4; ++j) acc[i][4 * j4 + j] = fmaf(ar[i], vr[j], acc[i][4 * j4 + j]);
+        }
       }
     }
+  } else {
+  float4 pre[kPi2Ahead];
+#pragma unroll
+  for (int u = 0; u < kPi2Ahead; ++u) pre[u] = pi2_load_a<VEC>(a, d, ks + kPi2Splits * u, row0, r4, nr);
+  for (int k0 = ks; k0 < d; k0 += kPi2Splits * kPi2Ahead) {
+#pragma unroll
+    for (int u = 0; u < kPi2Ahead; ++u) {
+      const int k = k0 + kPi2Splits * u;
+      const float4 av = pre[u];
+      pre[u] = pi2_load_a<VEC>(a, d, k + kPi2Splits * kPi2Ahead, row0, r4, nr);
+      const float4* vk = reinterpret_cast<const float4*>(v + (k < d ? k : 0) * kPiPool + ch * kPi2Cols);
+      const float ar[4] = {av.x, av.y, av.z, av.w};  // zero when k >= d
+#pragma unroll
+      for (int j4 = 0; j4 < kPi2Cols / 4; ++j4) {
+        const float4 vv = vk[j4];
+        const float vr[4] = {vv.x, vv.y, vv.z, vv.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][4 * j4 + j] = fmaf(ar[i], vr[j], acc[i][4 * j4 + j]);
+      }
+    }
+  }
+  }
+  // partials [split][row][16] -> fixed-order sum over the splits (+ eps V)
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float4* dst = reinterpret_cast<float4*>(red + (ks * kPi2R + r4 + i) * kPiPool + ch * kPi2Cols);
+#pragma unroll
+    for (int j4 = 0; j4 < kPi2Cols / 4; ++j4)
+      dst[j4] = make_float4(acc[i][4 * j4], acc[i][4 * j4 + 1], acc[i][4 * j4 + 2], acc[i][4 * j4 + 3]);
+  }
+  __syncthreads();
+  for (int e = t; e < nr * kPiPool; e += kPi2Threads) {
+    float x = 0.f;
+#pragma unroll
+    for (int s2 = 0; s2 < kPi2Splits; ++s2) x += red[s2 * kPi2R * kPiPool + e];
+    w[e] = fmaf(eps, v[row0 * kPiPool + e], x);
   }
   __syncthreads();
 }
@@ -492,21 +508,21 @@ __global__ void __launch_bounds__(kPi2Threads, 1) pi2_kernel(const float* __rest
                                                              int iters, unsigned long long seed,
                                                              float* __restrict__ scale, float* __restrict__ inv_scale,
                                                              int* __restrict__ status,
-                                                             const int* __restrict__ seed_index) {
+                                                             const int* __restrict__ seed_index, int exp_flags) {
   cg::cluster_group cl = cg::this_cluster();
   const int C = static_cast<int>(cl.num_blocks());
   const int q = static_cast<int>(cl.block_rank());
   const int m = blockIdx.x / C;
-  const int R = (d + C - 1) / C;
+  const int R = ((d + C - 1) / C + 3) / 4 * 4;  // rows per CTA, a multiple of 4 (16-byte aligned slabs)
+  const bool vec = d % 4 == 0;
   const int row0 = q * R;
   const int nr = max(0, min(R, d - row0));
   extern __shared__ __align__(16) unsigned char pi2_raw[];
   float* vbuf = reinterpret_cast<float*>(pi2_raw);                 // [2][d][16]
-  float* tiles = vbuf + 2 * d * kPiPool;                            // [2][KT][R]
-  float* w = tiles + 2 * kPi2KT * kPi2R;                            // [R][16]
-  float* red = w + kPi2R * kPiPool;                                 // [128][16]
-  double* stripes = reinterpret_cast<double*>(red + 128 * kPiPool);  // [16][16]
-  double* slots = stripes + 16 * kPiPool;                           // [8][16]
+  float* red = vbuf + 2 * d * kPiPool;                              // [splits][R][16]
+  float* w = red + kPi2Splits * kPi2R * kPiPool;                    // [R][16]
+  double* stripes = reinterpret_cast<double*>(w + kPi2R * kPiPool);  // [16][16]
+  double* slots = stripes + kPi2Threads;                            // [8][16]
   double* colv = slots + 8 * kPiPool;                               // [16]
   double* qv = colv + kPiPool;                                      // [16]
   double* vv = qv + kPiPool;                                        // [16]
@@ -546,7 +562,13 @@ __global__ void __launch_bounds__(kPi2Threads, 1) pi2_kernel(const float* __rest
     for (int it = 0; it < iters; ++it) {
       const float* vc = vbuf + cur * d * kPiPool;
       float* vn = vbuf + (cur ^ 1) * d * kPiPool;
-      pi2_matvec(a, d, eps, row0, nr, vc, tiles, w, red);
+      if (exp_flags & 1) {  // experiment: skip the matvec (W = V)
+        for (int i = threadIdx.x; i < nr * kPiPool; i += kPi2Threads) w[i] = vc[row0 * kPiPool + i];
+        __syncthreads();
+      } else {
+        if (vec) pi2_matvec<true>(a, d, eps, row0, nr, vc, red, w);
+        else pi2_matvec<false>(a, d, eps, row0, nr, vc, red, w);
+      }
       pi2_colsum(cl, C, q, w, kPiPool, nullptr, nr, stripes, slots, colv);
       for (int i = threadIdx.x; i < nr * kPiPool; i += kPi2Threads) {
         const double n = sqrt(colv[i % kPiPool]);
@@ -557,7 +579,8 @@ __global__ void __launch_bounds__(kPi2Threads, 1) pi2_kernel(const float* __rest
       cur ^= 1;
     }
     const float* vc = vbuf + cur * d * kPiPool;
-    pi2_matvec(a, d, eps, row0, nr, vc, tiles, w, red);  // A V once more for the quotients
+    if (vec) pi2_matvec<true>(a, d, eps, row0, nr, vc, red, w);  // A V once more for the quotients
+    else pi2_matvec<false>(a, d, eps, row0, nr, vc, red, w);
     pi2_colsum(cl, C, q, vc + row0 * kPiPool, kPiPool, w, nr, stripes, slots, qv);
     pi2_colsum(cl, C, q, vc + row0 * kPiPool, kPiPool, nullptr, nr, stripes, slots, vv);
     // every CTA evaluates the (identical) selection; rank 0 writes the result
@@ -614,8 +637,9 @@ static int pi2_launch(const float* ema, int n, int d, float eps, int pool, int i
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
+  static const int exp_flags = getenv("DASH_PI_EXP") ? atoi(getenv("DASH_PI_EXP")) : 0;  // experiment knob
   cudaError_t e = cudaLaunchKernelEx(&cfg, pi2_kernel, ema, d, eps, pool, iters, seed, scale, inv_scale, status,
-                                     seed_index);
+                                     seed_index, exp_flags);
   note_launch();
   return e == cudaSuccess ? DASH_OK : DASH_ECUDA;
 }
