@@ -32,6 +32,8 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "DASH optimizer step ms at 1/2/4/8 B200; Newton-DB batched solver TFLOP/s"
+SOLVER_DESC = {"ndb": "Newton-DB p=4/2 fixed {k} iters/chain", "cn": "coupled Newton p=4/2 fixed {k} iters",
+               "cbshv": "Chebyshev/Clenshaw degree 60"}
 
 
 def workload_shapes(name: str):
@@ -40,15 +42,24 @@ def workload_shapes(name: str):
     return {"llama953m": (llama_953m(), 1024), "llama124m": (llama_124m(), 1024), "c1": (C1, 256)}[name]
 
 
-def solver_flops(shapes, bsz: int, iters: int) -> dict:
-    """Algorithmic FLOPs per step: 2 r^2 c + 2 c^2 r stats/apply, NDB 1+3(k-1) products."""
+def solver_products(method: str, exponent: int, iters: int, degree: int = 60) -> int:
+    """Reference products per block: NDB 1+3(k-1) per chain (2 chains for p=4), CN 3k (p=2) /
+    4k (p=4), Clenshaw d-1."""
+    if method == "ndb":
+        return (2 if exponent == 4 else 1) * (1 + 3 * (iters - 1))
+    if method == "cn":
+        return (4 if exponent == 4 else 3) * iters
+    return degree - 1
+
+
+def solver_flops(shapes, bsz: int, iters: int, method: str = "ndb") -> dict:
+    """Algorithmic FLOPs per step: 2 r^2 c + 2 c^2 r stats/apply, 2 B^3 per solver product."""
     from paper_2602_02016_b200.shampoo import build_layout
 
     layers, specs = build_layout(shapes, bsz)
     ndb = 0.0
     for g in specs:
-        chains = 2 if g.exponent == 4 else 1
-        ndb += len(g.members) * chains * (1 + 3 * (iters - 1)) * 2.0 * g.dim ** 3
+        ndb += len(g.members) * solver_products(method, g.exponent, iters) * 2.0 * g.dim ** 3
     stats = apply = 0.0
     for lay in layers:
         if lay.is_matrix:
@@ -111,7 +122,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU baseline (oracle port)
-def cpu_baseline(shapes, bsz, iters, budget_s: float = 20.0):
+def cpu_baseline(shapes, bsz, iters, budget_s: float = 20.0, method: str = "ndb"):
     """Time the float64 oracle (restatement of the reference step) on a bounded sample and extrapolate."""
     import threadpoolctl
 
@@ -121,7 +132,7 @@ def cpu_baseline(shapes, bsz, iters, budget_s: float = 20.0):
     rng = np.random.default_rng(0)
     params = [rng.standard_normal(s) * 0.02 for s in sample_shapes]
     grads = [rng.standard_normal(s) * 1e-3 for s in sample_shapes]
-    cfg = core.OracleConfig(block_size=bsz, method="ndb", tolerance=0.0, max_iters=iters)
+    cfg = core.OracleConfig(block_size=bsz, method=method, tolerance=0.0, max_iters=iters)
     times = []
     t_start = time.perf_counter()
     while True:
@@ -132,8 +143,8 @@ def cpu_baseline(shapes, bsz, iters, budget_s: float = 20.0):
         if time.perf_counter() - t_start > budget_s * 0.5 or len(times) >= 5:
             break
     t = statistics.median(times)
-    full = solver_flops(shapes, bsz, iters)
-    samp = solver_flops(sample_shapes, bsz, iters)
+    full = solver_flops(shapes, bsz, iters, method)
+    samp = solver_flops(sample_shapes, bsz, iters, method)
     scale = sum(full.values()) / sum(samp.values())
     info = threadpoolctl.threadpool_info()
     cores = max([i.get("num_threads", 1) for i in info] + [1])
@@ -142,8 +153,9 @@ def cpu_baseline(shapes, bsz, iters, budget_s: float = 20.0):
         "unit": "ms",
         "cores": cores,
         "kind": "port",
-        "sample": (f"oracle float64 step on one (2048,2048) layer (8 blocks of 1024, NDB fixed {iters} iters/chain, "
-                   f"PI 16x30), median {len(times)} runs = {t:.2f} s, extrapolated x{scale:.1f} by algorithmic FLOPs"),
+        "sample": (f"oracle float64 step on one (2048,2048) layer (8 blocks of 1024, "
+                   f"{SOLVER_DESC[method].format(k=iters)}, PI 16x30), median {len(times)} runs = {t:.2f} s, "
+                   f"extrapolated x{scale:.1f} by algorithmic FLOPs"),
     }
 
 
@@ -164,8 +176,8 @@ def run_dash(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     shapes, bsz = workload_shapes(args.workload)
     prec = {"f32": PrecisionMode.EMULATED32, "f16": PrecisionMode.F16}[args.precision]
-    cfg = ShampooConfig(block_size=bsz, solver=SolverConfig(method="ndb", tolerance=0.0, max_iters=args.iters,
-                                                            precision=prec))
+    cfg = ShampooConfig(block_size=bsz, solver=SolverConfig(method=args.solver, tolerance=0.0,
+                                                            max_iters=args.iters, precision=prec))
     gen = torch.Generator(device="cuda")
     gen.manual_seed(1234)
     params = [torch.randn(s, device="cuda", generator=gen) * 0.02 for s in shapes]
@@ -205,7 +217,9 @@ def run_dash(args):
                            ("refreshed", "applied", "apply")):
             phases[name] = round(sum(x.elapsed_time(y) for x, y in zip(events[a], events[b])) / args.steps, 3)
     n_gemm, gemm_ms, gemm_flops = _lib.gemm_timing_read()
+    per_launch = _lib.gemm_timing_list()
     _lib.gemm_timing(False)
+    gemm_issued = sum(x[2] for x in per_launch)
     launches = (_lib.launch_count() - launches0) // args.steps
     ms = ms_local
     if world > 1:
@@ -231,10 +245,11 @@ def run_dash(args):
         e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
         del state_e, out
 
-    fl = solver_flops(shapes, bsz, args.iters)
+    fl = solver_flops(shapes, bsz, args.iters, args.solver)
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = peaks.get("bf16_tflops_sustained", 1420.2)
     achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
+    issued_tf = gemm_issued / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
     traffic = None
     tr_file = ROOT / "profiles" / "r1_gemm_traffic.json"
     if tr_file.exists():
@@ -250,10 +265,11 @@ def run_dash(args):
         "higher_is_better": False,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "fp16x3-split products, fp32 accumulate/storage" if args.precision == "f32" else "fp16, fp32 acc",
+        "dtype": ("fp16x3-split products (hi*hi + hi*lo + lo*hi), fp32 accumulate/storage" if args.precision == "f32"
+                  else "fp16 products, fp32 accumulate/storage"),
         "data": "synthetic (params N(0,0.02^2), grads N(0,1e-3^2), seeded)",
         "config": {
-            "workload": f"{args.workload} DASH step, B={bsz}, Newton-DB p=4/2 fixed {args.iters} iters/chain, "
+            "workload": f"{args.workload} DASH step, B={bsz}, {SOLVER_DESC[args.solver].format(k=args.iters)}, "
                         f"PI scaling (pool 16 x 30 iters), update_freq=1, grafting beta2=0.999",
             "params": int(sum(int(np.prod(s)) for s in shapes)),
             "precond_blocks": None,
@@ -264,8 +280,15 @@ def run_dash(args):
         "solver_tflops_per_s": None,
         "roofline": {
             "bound": "tensor",
-            "kernel": "dash_gemm_kernel<3> (tcgen05 split-f16 grouped GEMM; stats + NDB + apply launches)",
+            "kernel": (f"dash_gemm2_kernel<{3 if args.precision == 'f32' else 1}> (tcgen05 cta_group::2 grouped GEMM; "
+                       "stats + solver + apply launches)"),
             "achieved": round(achieved, 1),
+            "achieved_def": ("algorithmic: 2 M N K per reference product (solver blocks 2 B^3) / summed CUDA-event "
+                             "durations of the GEMM launches in the timed steps"),
+            "issued_tensor_tflops": round(issued_tf, 1),
+            "issued_frac": round(issued_tf / peak, 4),
+            "issued_def": ("fp16 tensor-core flops actually issued (tiles x 2 x 256 x 128 x padded K x passes; "
+                           "symmetric solver products run only the upper-triangle tiles) / the same durations"),
             "peak": peak,
             "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4),
@@ -287,7 +310,7 @@ def run_dash(args):
     if phases.get("refresh"):  # Newton-DB algorithmic FLOPs / refresh phase (includes PI, splits, rescale)
         result["solver_tflops_per_s"] = round(fl["ndb"] / world / (phases["refresh"] * 1e-3) / 1e12, 1)
     if rank == 0 and not args.no_cpu:
-        result["cpu_baseline"] = cpu_baseline(shapes, bsz, args.iters)
+        result["cpu_baseline"] = cpu_baseline(shapes, bsz, args.iters, method=args.solver)
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:
@@ -303,7 +326,7 @@ def run_reference(args):
     shapes, bsz = workload_shapes(args.workload)
     steps = []
     for _ in range(args.warmup + args.steps):
-        cb = cpu_baseline(shapes, bsz, args.iters, budget_s=8.0)
+        cb = cpu_baseline(shapes, bsz, args.iters, budget_s=8.0, method=args.solver)
         steps.append(cb)
     timed = steps[args.warmup:]
     v = statistics.median([c["value"] for c in timed])
@@ -321,7 +344,7 @@ def run_reference(args):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded)",
-        "config": {"workload": f"{args.workload} DASH step, B={bsz}, NDB fixed {args.iters} iters/chain, PI",
+        "config": {"workload": f"{args.workload} DASH step, B={bsz}, {SOLVER_DESC[args.solver].format(k=args.iters)}, PI",
                    "parallelism": "host CPU"},
         "cpu_baseline": {k: timed[-1][k] for k in ("kind", "cores", "sample")} | {"value": round(v, 1), "unit": "ms"},
         "e2e": {"value": round(v, 1), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -337,6 +360,7 @@ def main():
     ap.add_argument("--workload", default="llama953m", choices=["llama953m", "llama124m", "c1"])
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--precision", default="f32", choices=["f32", "f16"])
+    ap.add_argument("--solver", default="ndb", choices=["ndb", "cn", "cbshv"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

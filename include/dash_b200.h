@@ -55,9 +55,10 @@ int dash_device_sms(void);
 unsigned long long dash_launch_count(void);
 void dash_gemm_timing(int enable);
 int dash_gemm_timing_read(int* launches, double* ms, double* flops);
-/* Per-launch detail of the timed GEMM launches: up to `cap` (ms, algorithmic flops, tiles) triples;
- * returns the number written (or -status on error). */
-int dash_gemm_timing_list(int cap, double* ms, double* flops, int* tiles);
+/* Per-launch detail of the timed GEMM launches: up to `cap` entries of (ms, algorithmic flops = 2 M N K per
+ * job, issued tensor-core flops = tiles x 2 x 256 x 128 x padded K x passes, tiles); returns the number
+ * written (or -status on error). */
+int dash_gemm_timing_list(int cap, double* ms, double* flops, double* issued, int* tiles);
 
 /* ---------------------------------------------------------------- dense primitives (linalg.py)
  * dash_split: fp32 stack (src[m*src_mat_stride + r*src_ld + c]) -> split-f16 stack.

@@ -51,7 +51,7 @@ _SIGNATURES: dict[str, tuple] = {
     "dash_gemm_timing": (None, [c_int]),
     "dash_gemm_timing_read": (c_int, [ctypes.POINTER(c_int), ctypes.POINTER(ctypes.c_double),
                                       ctypes.POINTER(ctypes.c_double)]),
-    "dash_gemm_timing_list": (c_int, [c_int, c_void_p, c_void_p, c_void_p]),
+    "dash_gemm_timing_list": (c_int, [c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
     "dash_split": (c_int, [c_void_p, c_longlong, c_int, _P, c_void_p]),
     "dash_unsplit": (c_int, [_P, c_void_p, c_longlong, c_int, c_void_p]),
     "dash_bmm_ws_bytes": (c_size_t, [c_int]),
@@ -146,12 +146,13 @@ def gemm_timing_read() -> tuple[int, float, float]:
     return n.value, ms.value, fl.value
 
 
-def gemm_timing_list(cap: int = 65536) -> list[tuple[float, float, int]]:
-    """Per-launch (ms, algorithmic flops, tiles) of the GEMM launches since timing was enabled."""
+def gemm_timing_list(cap: int = 65536) -> list[tuple[float, float, float, int]]:
+    """Per-launch (ms, algorithmic flops, issued tensor flops, tiles) of the GEMM launches since timing
+    was enabled."""
     import numpy as np
 
-    ms, fl, tl = np.zeros(cap), np.zeros(cap), np.zeros(cap, dtype=np.int32)
-    n = lib().dash_gemm_timing_list(cap, ms.ctypes.data, fl.ctypes.data, tl.ctypes.data)
+    ms, fl, iss, tl = np.zeros(cap), np.zeros(cap), np.zeros(cap), np.zeros(cap, dtype=np.int32)
+    n = lib().dash_gemm_timing_list(cap, ms.ctypes.data, fl.ctypes.data, iss.ctypes.data, tl.ctypes.data)
     if n < 0:
         check(-n, "dash_gemm_timing_list")
-    return [(float(ms[i]), float(fl[i]), int(tl[i])) for i in range(n)]
+    return [(float(ms[i]), float(fl[i]), float(iss[i]), int(tl[i])) for i in range(n)]

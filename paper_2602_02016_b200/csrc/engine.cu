@@ -178,6 +178,7 @@ bool JobBuilder::operands(GemmJob& j, const dash_stack& a, int am, int trans_a, 
   j.b_amax = b.amax + bm;
   j.alpha = 1.f;
   j.c_map = j.c_tmap = j.c2_map = j.c2_tmap = -1;
+  j.s_map = -1;
   return true;
 }
 
@@ -192,6 +193,17 @@ void JobBuilder::set_out(GemmJob& j, const dash_stack& c, int cm) {
   j.c_mat = cm;
   j.c_map = add_map(c, 32, 64, 2, true);
   j.c_tmap = add_map(c, 64, 32, 2, false);
+}
+
+void JobBuilder::set_side(GemmJob& j, const dash_stack& s, int m) {
+  j.s_hi = reinterpret_cast<const __half*>(s.data) + static_cast<long long>(m) * 2 * s.rows * s.ld;
+  j.s_plane = static_cast<long long>(s.rows) * s.ld;
+  j.s_ld = s.ld;
+  j.s_exp = s.exp + m;
+  j.s_amax = s.amax + m;
+  j.s_mat = m;
+  static const int no_tma = getenv("DASH_NO_TMA_STORE") ? atoi(getenv("DASH_NO_TMA_STORE")) : 0;
+  j.s_map = no_tma ? -1 : add_map(s, 32, 64, 2, true);
 }
 
 void JobBuilder::set_out2(GemmJob& j, const dash_stack& c, int cm) {
@@ -246,7 +258,15 @@ bool JobBuilder::upload(Arena& ar, cudaStream_t st, UploadedGemm* out) {
   out->flops = 0.0;
   for (const GemmJob& j : jobs) out->flops += 2.0 * j.M * static_cast<double>(j.N) * j.K;
   out->uniform = uniform_tiles();
+  out->issued1 = issued_per_pass();
   return true;
+}
+
+double JobBuilder::issued_per_pass() const {
+  double f = 0.0;
+  for (const GemmJob& j : jobs)
+    f += static_cast<double>(job_tiles(j)) * 2.0 * kTileM * kTileN * ((j.K + kTileK - 1) / kTileK) * kTileK;
+  return f;
 }
 
 int JobBuilder::uniform_tiles() const {
@@ -295,7 +315,8 @@ int JobBuilder::launch(void* ws, size_t ws_bytes, int passes, cudaStream_t st) {
     return DASH_ECUDA;
   double fl = 0.0;
   for (const GemmJob& j : jobs) fl += 2.0 * j.M * static_cast<double>(j.N) * j.K;
-  return gemm_launch(d_jobs, static_cast<int>(jobs.size()), tiles, d_maps, passes, st, nullptr, fl, uniform_tiles());
+  return gemm_launch(d_jobs, static_cast<int>(jobs.size()), tiles, d_maps, passes, st, nullptr, fl, uniform_tiles(),
+                     issued_per_pass() * passes);
 }
 
 }  // namespace dash
@@ -314,9 +335,9 @@ int dash_gemm_timing_read(int* launches, double* ms, double* flops) {
   return gemm_timing_read(launches, ms, flops);
 }
 
-int dash_gemm_timing_list(int cap, double* ms, double* flops, int* tiles) {
-  if (cap < 0 || (cap > 0 && (!ms || !flops || !tiles))) return -DASH_EINVAL;
-  return gemm_timing_list(cap, ms, flops, tiles);
+int dash_gemm_timing_list(int cap, double* ms, double* flops, double* issued, int* tiles) {
+  if (cap < 0 || (cap > 0 && (!ms || !flops || !issued || !tiles))) return -DASH_EINVAL;
+  return gemm_timing_list(cap, ms, flops, issued, tiles);
 }
 
 int dash_device_sms(void) {

@@ -18,12 +18,13 @@ int job_tiles(const GemmJob& j);  // tiles the kernel runs for one job (fewer wh
 int split_stack(const float* src, long long mat_stride, int src_ld, const dash_stack& d, cudaStream_t st);
 int unsplit_stack(const dash_stack& s, float* dst, long long mat_stride, int dst_ld, cudaStream_t st);
 int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtensorMap* d_maps, int passes,
-                cudaStream_t stream, const int* gate = nullptr, double flops = 0.0, int uniform = 0);
+                cudaStream_t stream, const int* gate = nullptr, double flops = 0.0, int uniform = 0,
+                double issued = 0.0);
 void note_launch(int n = 1);  // count non-GEMM kernel launches
 extern unsigned long long g_launches;
 void gemm_timing_enable(int on);
 int gemm_timing_read(int* n, double* ms, double* flops);
-int gemm_timing_list(int cap, double* ms, double* flops, int* tiles);
+int gemm_timing_list(int cap, double* ms, double* flops, double* issued, int* tiles);
 
 // A grouped GEMM whose maps + jobs already live in device memory.
 struct UploadedGemm {
@@ -31,9 +32,10 @@ struct UploadedGemm {
   const CUtensorMap* maps = nullptr;
   int njobs = 0, tiles = 0;
   int uniform = 0;     // tiles per job when all jobs have the same count (O(1) tile -> job), else 0
-  double flops = 0.0;  // algorithmic: sum over jobs of 2 M N K
+  double flops = 0.0;   // algorithmic: sum over jobs of 2 M N K
+  double issued1 = 0.0; // tensor-core flops issued per pass (tiles x 2 x 256 x 128 x padded K)
   int run(int passes, cudaStream_t st, const int* gate = nullptr) const {
-    return njobs ? gemm_launch(jobs, njobs, tiles, maps, passes, st, gate, flops, uniform) : 0;
+    return njobs ? gemm_launch(jobs, njobs, tiles, maps, passes, st, gate, flops, uniform, issued1 * passes) : 0;
   }
 };
 
@@ -84,10 +86,12 @@ struct JobBuilder {
                 bool check = true);
   void set_out(GemmJob& j, const dash_stack& c, int cm);
   void set_out2(GemmJob& j, const dash_stack& c, int cm);  // second split output (EPI_CN_M correction)
+  void set_side(GemmJob& j, const dash_stack& s, int m);   // split side input (EPI_CHEB*: B_{k+2})
   void push(GemmJob& j);
   static size_t bytes_for(int nmaps, int njobs);
   int launch(void* ws, size_t ws_bytes, int passes, cudaStream_t st);
   int uniform_tiles() const;
+  double issued_per_pass() const;
   // Upload maps + jobs into the arena (one H2D copy); the builder may be reused afterwards.
   bool upload(Arena& ar, cudaStream_t st, UploadedGemm* out);
   size_t upload_bytes() const { return bytes_for(static_cast<int>(maps.size()), static_cast<int>(jobs.size())); }

@@ -161,6 +161,8 @@ struct EpiCtx {
   float amax, amax2, resid;
   double sumsq;
   bool ovf, ovf2;
+  const uint8_t* sbuf;  // side input tile staged in shared memory by TMA (direct swizzled layout) or null
+  int lane, lc0;        // lane (= row within the warp tile) and first column of the warp tile
 };
 
 template <int W>
@@ -236,12 +238,36 @@ __device__ __forceinline__ void epi_piece(const GemmJob& jb, EpiCtx& cx, int c0,
     case EPI_CHEB:
     case EPI_CHEB_FINAL: {
       const bool fin = cx.op == EPI_CHEB_FINAL;
-      const __half* sh = jb.s_hi + static_cast<long long>(r) * jb.s_ld + c0;
-      const __half* sl = sh + jb.s_plane;
+      __half svh[W], svl[W];
+      if (cx.sbuf) {  // W consecutive columns = W / 8 swizzled 16-byte chunks of this lane's row
+#pragma unroll
+        for (int c8 = 0; c8 < W / 8; ++c8) {
+          const int ch = (c0 - cx.lc0) / 8 + c8;
+          const int off = cx.lane * 128 + ((ch ^ (cx.lane & 7)) << 4);
+          const uint4 h = *reinterpret_cast<const uint4*>(cx.sbuf + off);
+          const uint4 l = *reinterpret_cast<const uint4*>(cx.sbuf + 4096 + off);
+          const __half* hp = reinterpret_cast<const __half*>(&h);
+          const __half* lp = reinterpret_cast<const __half*>(&l);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            svh[8 * c8 + e] = hp[e];
+            svl[8 * c8 + e] = lp[e];
+          }
+        }
+      } else {
+        const __half* sh = jb.s_hi + static_cast<long long>(r) * jb.s_ld + c0;
+        const __half* sl = sh + jb.s_plane;
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+          const bool ok = cx.row_ok && c0 + i < cx.N;
+          svh[i] = ok ? sh[i] : __float2half(0.f);
+          svl[i] = ok ? sl[i] : __float2half(0.f);
+        }
+      }
 #pragma unroll
       for (int i = 0; i < W; ++i) {
         float sv = 0.f;
-        if (cx.row_ok && c0 + i < cx.N) sv = (__half2float(sh[i]) + __half2float(sl[i])) * cx.side_scale;
+        if (cx.row_ok && c0 + i < cx.N) sv = (__half2float(svh[i]) + __half2float(svl[i])) * cx.side_scale;
         const float d = (r == c0 + i) ? cx.gam : 0.f;
         const float y = fin ? (x[i] * cx.sc - sv + d) * cx.mul : 2.f * (x[i] * cx.sc) - sv + d;
         x[i] = y;
@@ -339,7 +365,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + kSlots;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kSlots);
+  uint64_t* sbar = tempty + kSlots;  // per epilogue warp: side-input TMA load
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbar + kEpiWarps);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
@@ -355,6 +382,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       mbar_init(&tfull[a], 1);                // pair-MMA commit (multicast)
       mbar_init(&tempty[a], 2 * kEpiWarps);   // every epilogue warp of both CTAs (leader's copy used)
     }
+    for (int w = 0; w < kEpiWarps; ++w) mbar_init(&sbar[w], 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc2<kSlots * kPairN>(tmem_slot);
@@ -462,6 +490,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     const int q = warp & 3;                         // TMEM lane quarter (warps 2..9 -> 2, 3, 0, 1, 2, 3, 0, 1)
     const int hc = static_cast<int>(warp - 2) >> 2;  // column half (64 columns) of this warp
     uint8_t* ebuf = smem + C::kStages * C::kStageBytes + (warp - 2) * 8192;  // 1024-aligned staging tile
+    uint32_t sphase = 0;
     const uint32_t leader_tempty = mapa_shared(smem_u32(tempty), 0);
     uint32_t t = 0;
     for (int tile = pair; tile < total_tiles; tile += npairs, ++t) {
@@ -476,6 +505,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       const int used = (nk + per - 1) / per;
       const uint32_t base = (t % nsets) * static_cast<uint32_t>(nacc);
       const uint32_t use_par = (t / nsets) & 1u;
+      const bool side_tma = jb.s_map >= 0;
+      __syncwarp();                 // every lane is done with the previous tile's staging buffer
+      if (side_tma && lane == 0) {  // stage the side input tile while the MMAs run
+        bulk_wait_read0();          // the previous tile's bulk stores have read the buffer
+        mbar_arrive_expect_tx(&sbar[warp - 2], 8192);
+        tma_load_4d(ebuf, maps + jb.s_map, &sbar[warp - 2], n0 + 64 * hc,
+                    m0 + kHalf * static_cast<int>(rank) + 32 * q, 0, jb.s_mat);
+      }
       float acc[64];
       for (int c = 0; c < nacc; ++c) {
         const uint32_t slot = base + static_cast<uint32_t>(c);
@@ -538,6 +575,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       cx.sumsq = 0.0;
       cx.ovf = cx.ovf2 = false;
       const bool tma_out = jb.c_map >= 0;
+      cx.sbuf = nullptr;
+      cx.lane = static_cast<int>(lane);
+      cx.lc0 = n0 + 64 * hc;
+      if (side_tma) {
+        mbar_wait(&sbar[warp - 2], sphase);
+        sphase ^= 1u;
+        cx.sbuf = ebuf;
+      }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int c0 = n0 + 64 * hc + 16 * j;
@@ -551,11 +596,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         const int lr = static_cast<int>(lane);
         auto ident = [](float v, int) { return v; };
         if (lane == 0) bulk_wait_read0();  // this warp's previous stores have read the buffer
-        __syncwarp();
-        stage_direct(ebuf, acc, lr, c0, cx.inv_out, ident, cx.ovf);
+        __syncwarp();                      // (and every lane is done with the staged side input)
+        if (!(xp & 4)) stage_direct(ebuf, acc, lr, c0, cx.inv_out, ident, cx.ovf);
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) {
+        if (lane == 0 && !(xp & 8)) {
           tma_store_4d(maps + jb.c_map, ebuf, c0, r0, 0, jb.c_mat);
           bulk_commit();
         }
@@ -639,7 +684,7 @@ static int g_exp = -1;
 struct GemmTimer {
   bool on = false;
   std::vector<cudaEvent_t> ev;  // start/stop pairs
-  std::vector<double> flops;
+  std::vector<double> flops, issued;
   std::vector<int> tiles;
   size_t used = 0;
 };
@@ -649,7 +694,7 @@ unsigned long long g_launches = 0;
 void note_launch(int n) { g_launches += static_cast<unsigned long long>(n); }
 
 int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtensorMap* d_maps, int passes,
-                cudaStream_t stream, const int* gate, double flops, int uniform) {
+                cudaStream_t stream, const int* gate, double flops, int uniform, double issued) {
   if (total_tiles <= 0) return 0;
   ++g_launches;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -665,6 +710,7 @@ int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtenso
     e1 = g_timer.ev[g_timer.used + 1];
     g_timer.used += 2;
     g_timer.flops.push_back(flops);
+    g_timer.issued.push_back(issued);
     g_timer.tiles.push_back(total_tiles);
     cudaEventRecord(e0, stream);
   }
@@ -716,10 +762,11 @@ void gemm_timing_enable(int on) {
   g_timer.on = on != 0;
   g_timer.used = 0;
   g_timer.flops.clear();
+  g_timer.issued.clear();
   g_timer.tiles.clear();
 }
 
-int gemm_timing_list(int cap, double* ms, double* flops, int* tiles) {
+int gemm_timing_list(int cap, double* ms, double* flops, double* issued, int* tiles) {
   const int k = static_cast<int>(g_timer.used / 2);
   const int n = k < cap ? k : cap;
   for (int i = 0; i < n; ++i) {
@@ -728,6 +775,7 @@ int gemm_timing_list(int cap, double* ms, double* flops, int* tiles) {
     cudaEventElapsedTime(&x, g_timer.ev[2 * i], g_timer.ev[2 * i + 1]);
     ms[i] = x;
     flops[i] = g_timer.flops[i];
+    issued[i] = g_timer.issued[i];
     tiles[i] = g_timer.tiles[i];
   }
   return n;

@@ -634,13 +634,6 @@ size_t cheb_ws_bytes(int n, int b) {
 
 __global__ void pick_scalar_kernel(float* dst, const float* src, int k) { *dst = src[k]; }
 
-static void side_input(GemmJob& j, const dash_stack& sd, int m) {
-  j.s_hi = reinterpret_cast<const __half*>(sd.data) + static_cast<long long>(m) * 2 * sd.rows * sd.ld;
-  j.s_plane = static_cast<long long>(sd.rows) * sd.ld;
-  j.s_ld = sd.ld;
-  j.s_exp = sd.exp + m;
-  j.s_amax = sd.amax + m;
-}
 
 int cheb_solve(const dash_stack& a, const float* inv_scale, const float* mult, const double* coeffs, int degree,
                float* f_out, const dash_stack* out_split, int passes, void* ws, size_t ws_bytes, cudaStream_t st) {
@@ -669,7 +662,7 @@ int cheb_solve(const dash_stack& a, const float* inv_scale, const float* mult, c
       j.out_mat = m;
       j.sym = 1;
       j.gamma_p = cur;
-      side_input(j, bb[(r + 2) % 3], m);
+      jb.set_side(j, bb[(r + 2) % 3], m);
       jb.set_out(j, bb[r], m);
       jb.push(j);
     }
@@ -685,7 +678,7 @@ int cheb_solve(const dash_stack& a, const float* inv_scale, const float* mult, c
       j.sym = 1;
       j.gamma = hc[0];
       j.alpha_p = mult;
-      side_input(j, bb[2], m);
+      jb.set_side(j, bb[2], m);
       if (out_split) jb.set_out(j, *out_split, m);
       if (f_out) {
         j.f_out = f_out + static_cast<long long>(m) * a.rows * a.rows;

@@ -61,6 +61,7 @@ struct GemmJob {
   int c_map, c_tmap, c2_map, c2_tmap;
   int c_rows, c_cols;  // dims of the output stack (TMA stores only when the job covers it exactly)
   int c_mat, c2_mat;   // matrix index of the outputs within their stacks (TMA coordinate)
+  int s_map, s_mat;    // TMA load map (box 64 x 32 x 2 planes, 128-byte swizzle) + matrix of the side input, or -1
   // ---- split output (hi plane; lo plane at +c_plane elements)
   __half* c_hi; long long c_plane; int* c_exp; unsigned* c_amax;
   // ---- second split output (EPI_CN_M correction factor)

@@ -30,7 +30,7 @@ def spd_stack(n: int, b: int, seed: int = 0) -> torch.Tensor:
 
 def report(tag: str, lst) -> None:
     agg = collections.OrderedDict()
-    for ms, fl, tiles in lst:
+    for ms, fl, _iss, tiles in lst:
         k = (tiles, fl)
         t = agg.setdefault(k, [0, 0.0])
         t[0] += 1
