@@ -43,6 +43,20 @@ bool make_stack_map(const dash_stack& s, int box_rows, CUtensorMap* out, int box
   return r == CUDA_SUCCESS;
 }
 
+bool make_f32_map(const float* base, int nmat, int rows, int ld, int box_cols, int box_rows, bool swz,
+                  CUtensorMap* out) {
+  auto fn = encode_fn();
+  if (!fn || ld % 4 != 0 || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(ld), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(nmat)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 4, static_cast<cuuint64_t>(rows) * ld * 4};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 bool stack_ok(const dash_stack* s) {
   return s && s->data && s->nmat > 0 && s->rows > 0 && s->cols > 0 && s->ld >= s->cols && s->ld % kLdAlign == 0 &&
          s->exp && s->amax;
@@ -179,6 +193,7 @@ bool JobBuilder::operands(GemmJob& j, const dash_stack& a, int am, int trans_a, 
   j.alpha = 1.f;
   j.c_map = j.c_tmap = j.c2_map = j.c2_tmap = -1;
   j.s_map = -1;
+  j.f_map = j.f_tmap = -1;
   return true;
 }
 
@@ -193,6 +208,33 @@ void JobBuilder::set_out(GemmJob& j, const dash_stack& c, int cm) {
   j.c_mat = cm;
   j.c_map = add_map(c, 32, 64, 2, true);
   j.c_tmap = add_map(c, 64, 32, 2, false);
+}
+
+int JobBuilder::add_f32_map(const float* base, int nmat, int rows, int ld, int box_cols, int box_rows, bool swz) {
+  for (size_t i = 0; i < map_keys.size(); ++i) {
+    const MapKey& k = map_keys[i];
+    if (k.data == base && k.planes == -1 && k.box == box_rows && k.box_cols == box_cols && k.swz == swz &&
+        k.nmat == nmat && k.rows == rows && k.ld == ld)
+      return static_cast<int>(i);
+  }
+  CUtensorMap m;
+  if (!make_f32_map(base, nmat, rows, ld, box_cols, box_rows, swz, &m)) return -1;
+  maps.push_back(m);
+  map_keys.push_back(MapKey{base, box_rows, nmat, rows, ld, box_cols, -1, swz});
+  return static_cast<int>(maps.size()) - 1;
+}
+
+void JobBuilder::set_fout(GemmJob& j, float* base, int nmat, int rows, int ld, int mat, bool is_input) {
+  j.f_out = base + static_cast<long long>(mat) * rows * ld;
+  j.f_ld = ld;
+  if (is_input) j.f_in = j.f_out;
+  j.f_mat = mat;
+  j.f_rows = rows;
+  j.f_cols = ld;
+  static const int no_tma = getenv("DASH_NO_TMA_STORE") ? atoi(getenv("DASH_NO_TMA_STORE")) : 0;
+  j.f_map = no_tma ? -1 : add_f32_map(base, nmat, rows, ld, 32, 32, true);
+  j.f_tmap = no_tma ? -1 : add_f32_map(base, nmat, rows, ld, 32, 64, false);
+  if (j.f_map < 0 || j.f_tmap < 0) j.f_map = j.f_tmap = -1;
 }
 
 void JobBuilder::set_side(GemmJob& j, const dash_stack& s, int m) {

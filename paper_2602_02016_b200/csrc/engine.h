@@ -87,6 +87,9 @@ struct JobBuilder {
   void set_out(GemmJob& j, const dash_stack& c, int cm);
   void set_out2(GemmJob& j, const dash_stack& c, int cm);  // second split output (EPI_CN_M correction)
   void set_side(GemmJob& j, const dash_stack& s, int m);   // split side input (EPI_CHEB*: B_{k+2})
+  // fp32 output matrix `mat` of a contiguous (nmat, rows, ld) stack (EPI_EMA: also the input), TMA-staged
+  void set_fout(GemmJob& j, float* base, int nmat, int rows, int ld, int mat, bool is_input = false);
+  int add_f32_map(const float* base, int nmat, int rows, int ld, int box_cols, int box_rows, bool swz);
   void push(GemmJob& j);
   static size_t bytes_for(int nmaps, int njobs);
   int launch(void* ws, size_t ws_bytes, int passes, cudaStream_t st);

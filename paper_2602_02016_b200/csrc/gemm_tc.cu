@@ -162,8 +162,16 @@ struct EpiCtx {
   double sumsq;
   bool ovf, ovf2;
   const uint8_t* sbuf;  // side input tile staged in shared memory by TMA (direct swizzled layout) or null
+  const uint8_t* fbuf;  // EPI_EMA: fp32 input tile staged by TMA ([2][32 rows][32 floats], swizzled) or null
+  bool f_tma;           // fp32 output goes through the staged bulk store (skip direct stores)
   int lane, lc0;        // lane (= row within the warp tile) and first column of the warp tile
 };
+
+// fp32 tile staging: [half][32 rows][32 floats], 128-byte swizzle (two {32, 32, 1} boxes per 64-column tile).
+__device__ __forceinline__ int f32_off(int lane, int col) {  // col in [0, 64)
+  const int h = col >> 5, w = col & 31;
+  return h * 4096 + lane * 128 + (((w >> 2) ^ (lane & 7)) << 4) + (w & 3) * 4;
+}
 
 template <int W>
 __device__ __forceinline__ void put_split(const EpiCtx& cx, __half* hi, long long plane, int ld, int c0,
@@ -197,7 +205,7 @@ __device__ __forceinline__ void epi_piece(const GemmJob& jb, EpiCtx& cx, int c0,
         if (cx.row_ok && c0 + i < cx.N) cx.amax = nonneg_max(cx.amax, fabsf(x[i]));
       }
       if (jb.c_hi && split_now) put_split<W>(cx, jb.c_hi, jb.c_plane, jb.c_ld, c0, x, cx.inv_out, cx.ovf);
-      if (jb.f_out) put_f32<W>(cx, jb.f_out, jb.f_ld, c0, x);
+      if (jb.f_out && !cx.f_tma) put_f32<W>(cx, jb.f_out, jb.f_ld, c0, x);
     } break;
     case EPI_NDB_E: {
 #pragma unroll
@@ -214,23 +222,34 @@ __device__ __forceinline__ void epi_piece(const GemmJob& jb, EpiCtx& cx, int c0,
       if (split_now) put_split<W>(cx, jb.c_hi, jb.c_plane, jb.c_ld, c0, x, cx.inv_out, cx.ovf);
     } break;
     case EPI_EMA: {  // never symmetric (host); fp32 read-modify-write
-      if (cx.row_ok) {
+      const float b = jb.beta, omb = 1.f - jb.beta;
+      if (cx.fbuf) {   // staged input; the output is staged + bulk-stored by the caller (values stay in x)
+#pragma unroll
+        for (int i4 = 0; i4 < W / 4; ++i4) {
+          const float4 fi = *reinterpret_cast<const float4*>(cx.fbuf + f32_off(cx.lane, c0 - cx.lc0 + 4 * i4));
+          x[4 * i4] = b * fi.x + omb * (x[4 * i4] * cx.sc);
+          x[4 * i4 + 1] = b * fi.y + omb * (x[4 * i4 + 1] * cx.sc);
+          x[4 * i4 + 2] = b * fi.z + omb * (x[4 * i4 + 2] * cx.sc);
+          x[4 * i4 + 3] = b * fi.w + omb * (x[4 * i4 + 3] * cx.sc);
+        }
+      } else if (cx.row_ok) {
         const float* fi = jb.f_in + static_cast<long long>(r) * jb.f_ld + c0;
         float* fo = jb.f_out + static_cast<long long>(r) * jb.f_ld + c0;
-        const float b = jb.beta, omb = 1.f - jb.beta;
 #pragma unroll
         for (int i = 0; i < W; ++i)
           if (c0 + i < cx.N) fo[i] = b * fi[i] + omb * (x[i] * cx.sc);
       }
     } break;
     case EPI_APPLY: {  // never symmetric (host)
+#pragma unroll
+      for (int i = 0; i < W; ++i) x[i] *= cx.sc;
       if (cx.row_ok) {
         float* fo = jb.f_out + static_cast<long long>(r) * jb.f_ld + c0;
 #pragma unroll
         for (int i = 0; i < W; ++i)
           if (c0 + i < cx.N) {
-            const float u = x[i] * cx.sc;
-            fo[i] = u;
+            const float u = x[i];
+            if (!cx.f_tma) fo[i] = u;
             cx.sumsq += static_cast<double>(u) * u;
           }
       }
@@ -274,7 +293,7 @@ __device__ __forceinline__ void epi_piece(const GemmJob& jb, EpiCtx& cx, int c0,
         if (cx.row_ok && c0 + i < cx.N) cx.amax = nonneg_max(cx.amax, fabsf(y));
       }
       if (jb.c_hi && split_now) put_split<W>(cx, jb.c_hi, jb.c_plane, jb.c_ld, c0, x, cx.inv_out, cx.ovf);
-      if (jb.f_out) put_f32<W>(cx, jb.f_out, jb.f_ld, c0, x);
+      if (jb.f_out && !cx.f_tma) put_f32<W>(cx, jb.f_out, jb.f_ld, c0, x);
     } break;
     case EPI_CN_M: {
       float cc[W];
@@ -347,6 +366,20 @@ __device__ __forceinline__ void stage_transpose_in_place(uint8_t* buf, int lane)
     bh[j * 32] = static_cast<uint16_t>(hv[j >> 1] >> sh);
     bh[2048 + j * 32] = static_cast<uint16_t>(lv[j >> 1] >> sh);
   }
+}
+
+__device__ __forceinline__ void stage_direct_f32(uint8_t* buf, const float (&acc)[64], int lane) {
+#pragma unroll
+  for (int c4 = 0; c4 < 16; ++c4)
+    *reinterpret_cast<float4*>(buf + f32_off(lane, 4 * c4)) =
+        make_float4(acc[4 * c4], acc[4 * c4 + 1], acc[4 * c4 + 2], acc[4 * c4 + 3]);
+}
+
+// Transposed fp32 tile [64 rows (= columns)][32 floats (= this warp's rows)], no swizzle ({32, 64, 1} box).
+__device__ __forceinline__ void stage_transposed_f32(uint8_t* buf, const float (&acc)[64], int lane) {
+  float* b = reinterpret_cast<float*>(buf) + lane;
+#pragma unroll
+  for (int j = 0; j < 64; ++j) b[j * 32] = acc[j];
 }
 
 template <int PASSES>
@@ -506,12 +539,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       const uint32_t base = (t % nsets) * static_cast<uint32_t>(nacc);
       const uint32_t use_par = (t / nsets) & 1u;
       const bool side_tma = jb.s_map >= 0;
+      const bool f_tma = jb.f_map >= 0;
+      const bool fin_tma = f_tma && jb.op == EPI_EMA;
       __syncwarp();                 // every lane is done with the previous tile's staging buffer
-      if (side_tma && lane == 0) {  // stage the side input tile while the MMAs run
+      if ((side_tma || fin_tma) && lane == 0) {  // stage the side / fp32 input tile while the MMAs run
         bulk_wait_read0();          // the previous tile's bulk stores have read the buffer
         mbar_arrive_expect_tx(&sbar[warp - 2], 8192);
-        tma_load_4d(ebuf, maps + jb.s_map, &sbar[warp - 2], n0 + 64 * hc,
-                    m0 + kHalf * static_cast<int>(rank) + 32 * q, 0, jb.s_mat);
+        const int tc0 = n0 + 64 * hc, tr0 = m0 + kHalf * static_cast<int>(rank) + 32 * q;
+        if (side_tma) {
+          tma_load_4d(ebuf, maps + jb.s_map, &sbar[warp - 2], tc0, tr0, 0, jb.s_mat);
+        } else {
+          tma_load_3d(ebuf, maps + jb.f_map, &sbar[warp - 2], tc0, tr0, jb.f_mat);
+          tma_load_3d(ebuf + 4096, maps + jb.f_map, &sbar[warp - 2], tc0 + 32, tr0, jb.f_mat);
+        }
       }
       float acc[64];
       for (int c = 0; c < nacc; ++c) {
@@ -576,12 +616,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       cx.ovf = cx.ovf2 = false;
       const bool tma_out = jb.c_map >= 0;
       cx.sbuf = nullptr;
+      cx.fbuf = nullptr;
+      cx.f_tma = f_tma;
       cx.lane = static_cast<int>(lane);
       cx.lc0 = n0 + 64 * hc;
-      if (side_tma) {
+      if (side_tma || fin_tma) {
         mbar_wait(&sbar[warp - 2], sphase);
         sphase ^= 1u;
-        cx.sbuf = ebuf;
+        if (side_tma) cx.sbuf = ebuf;
+        else cx.fbuf = ebuf;
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -589,12 +632,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         float (&v)[16] = *reinterpret_cast<float(*)[16]>(&acc[16 * j]);  // in place: final values stay in acc
         if (c0 < jb.N && !(xp & 2)) epi_piece<16>(jb, cx, c0, v, !tma_out);
       }
-      if (tma_out && cx.store && !(xp & 2)) {
+      if ((tma_out || f_tma) && cx.store && !(xp & 2)) {
         // ---- staged bulk-tensor stores of the split output(s), direct and (symmetric jobs) mirrored
         const int r0 = m0 + kHalf * static_cast<int>(rank) + 32 * q;
         const int c0 = n0 + 64 * hc;
         const int lr = static_cast<int>(lane);
         auto ident = [](float v, int) { return v; };
+        if (tma_out) {
         if (lane == 0) bulk_wait_read0();  // this warp's previous stores have read the buffer
         __syncwarp();                      // (and every lane is done with the staged side input)
         if (!(xp & 4)) stage_direct(ebuf, acc, lr, c0, cx.inv_out, ident, cx.ovf);
@@ -640,6 +684,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             __syncwarp();
             if (lane == 0) {
               tma_store_4d(maps + jb.c2_tmap, ebuf, r0, c0, 0, jb.c2_mat);
+              bulk_commit();
+            }
+          }
+        }
+        }  // tma_out
+        if (f_tma) {  // fp32 output: direct tile (two swizzled 32 x 32 boxes) and, if symmetric, its mirror
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
+          stage_direct_f32(ebuf, acc, lr);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(maps + jb.f_map, ebuf, c0, r0, jb.f_mat);
+            tma_store_3d(maps + jb.f_map, ebuf + 4096, c0 + 32, r0, jb.f_mat);
+            bulk_commit();
+          }
+          if (cx.mirror) {
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+            stage_transposed_f32(ebuf, acc, lr);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_3d(maps + jb.f_tmap, ebuf, r0, c0, jb.f_mat);
               bulk_commit();
             }
           }

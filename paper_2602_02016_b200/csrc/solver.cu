@@ -680,10 +680,7 @@ int cheb_solve(const dash_stack& a, const float* inv_scale, const float* mult, c
       j.alpha_p = mult;
       jb.set_side(j, bb[2], m);
       if (out_split) jb.set_out(j, *out_split, m);
-      if (f_out) {
-        j.f_out = f_out + static_cast<long long>(m) * a.rows * a.rows;
-        j.f_ld = a.rows;
-      }
+      if (f_out) jb.set_fout(j, f_out, n, a.rows, a.rows, m);
       jb.push(j);
     }
     if (!jb.upload(ar, st, &g_fin)) return DASH_EINVAL;

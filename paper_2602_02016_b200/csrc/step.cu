@@ -803,9 +803,7 @@ dash_plan* dash_plan_create(const dash_block* blocks, int nb_m, int nb_v, int bl
     j.beta = beta_lr;
     {
       const int d = p->gdim[k.group_l];
-      j.f_out = p->gema[k.group_l] + static_cast<long long>(k.slot_l) * d * d;
-      j.f_in = j.f_out;
-      j.f_ld = d;
+      js.set_fout(j, p->gema[k.group_l], p->gsize[k.group_l], d, d, k.slot_l, true);
     }
     js.push(j);
     if (mat) {  // R
@@ -814,9 +812,7 @@ dash_plan* dash_plan_create(const dash_block* blocks, int nb_m, int nb_v, int bl
       j.op = EPI_EMA;
       j.beta = beta_lr;
       const int d = p->gdim[k.group_r];
-      j.f_out = p->gema[k.group_r] + static_cast<long long>(k.slot_r) * d * d;
-      j.f_in = j.f_out;
-      j.f_ld = d;
+      js.set_fout(j, p->gema[k.group_r], p->gsize[k.group_r], d, d, k.slot_r, true);
       js.push(j);
     }
     // ---- apply jobs
@@ -835,8 +831,7 @@ dash_plan* dash_plan_create(const dash_block* blocks, int nb_m, int nb_v, int bl
       set_dims(j, k.rows, k.cols, k.cols);
       j.op = EPI_APPLY;
       j.out_mat = b;
-      j.f_out = p->um + static_cast<long long>(b) * block_size * block_size;
-      j.f_ld = block_size;
+      j2.set_fout(j, p->um, p->nb_m, block_size, block_size, b);
       j.partial = p->un_part + static_cast<long long>(b) * p->un_stride;
       j2.push(j);
     } else {

@@ -62,6 +62,8 @@ struct GemmJob {
   int c_rows, c_cols;  // dims of the output stack (TMA stores only when the job covers it exactly)
   int c_mat, c2_mat;   // matrix index of the outputs within their stacks (TMA coordinate)
   int s_map, s_mat;    // TMA load map (box 64 x 32 x 2 planes, 128-byte swizzle) + matrix of the side input, or -1
+  int f_map, f_tmap, f_mat;  // fp32 output (and EPI_EMA input) maps: box 32 x 32 (128-byte swizzle) and 32 x 64
+  int f_rows, f_cols;        // (transposed mirror), or -1; f_rows x f_cols = dims of the fp32 matrices
   // ---- split output (hi plane; lo plane at +c_plane elements)
   __half* c_hi; long long c_plane; int* c_exp; unsigned* c_amax;
   // ---- second split output (EPI_CN_M correction factor)
