@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "engine.h"
+#include "elem.cuh"
 #include "ptx.cuh"
 #include "solver.h"
 
@@ -147,33 +148,25 @@ __global__ void ndb_first_kernel(dash_stack a, const float* __restrict__ inv_sca
   const int n = a.rows;
   const float sa = ldexpf(1.f, a.exp[m]) * (inv_scale ? inv_scale[m] : 1.f);
   const float inv_e = ldexpf(1.f, -kEExp);
-  const __half* ah = reinterpret_cast<const __half*>(a.data) + static_cast<long long>(m) * 2 * n * a.ld;
-  const __half* al = ah + static_cast<long long>(n) * a.ld;
-  __half* eh = reinterpret_cast<__half*>(e.data) + static_cast<long long>(m) * 2 * n * e.ld;
-  __half* el = eh + static_cast<long long>(n) * e.ld;
-  __half* zh = reinterpret_cast<__half*>(z.data) + static_cast<long long>(m) * 2 * n * z.ld;
-  __half* zl = zh + static_cast<long long>(n) * z.ld;
+  const __half* ah = mat_hi(a, m);
+  __half* eh = mat_hi(e, m);
+  __half* zh = mat_hi(z, m);
   float rmax = 0.f, amax = 0.f;
   bool ovf = false;
-  const long long total = static_cast<long long>(n) * n;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int r = static_cast<int>(i / n), c = static_cast<int>(i % n);
-    const long long oa = static_cast<long long>(r) * a.ld + c;
-    const float av = (__half2float(ah[oa]) + __half2float(al[oa])) * sa;
-    const float d = (r == c) ? 1.f : 0.f;
-    const float ev = 1.5f * d - 0.5f * av;
-    rmax = nonneg_max(rmax, fabsf(ev - d));
-    amax = nonneg_max(amax, fabsf(ev));
-    const float y = ev * inv_e;
-    const __half h = __float2half_rn(y);
-    const __half l = __float2half_rn(y - __half2float(h));
-    ovf |= __hisinf(h) || __hisnan(h);
-    const long long oe = static_cast<long long>(r) * e.ld + c;
-    eh[oe] = h; el[oe] = l;
-    const long long oz = static_cast<long long>(r) * z.ld + c;
-    zh[oz] = h; zl[oz] = l;
-  }
+  for_chunks8(n, a.ld, [&](int r, int c) {
+    float v[8];
+    load_split8(ah, mat_plane(a), static_cast<long long>(r) * a.ld + c, sa, v);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float d = (r == c + i) ? 1.f : 0.f;
+      const float ev = (c + i < n) ? 1.5f * d - 0.5f * v[i] : 0.f;
+      v[i] = ev;
+      rmax = nonneg_max(rmax, fabsf(ev - d));
+      amax = nonneg_max(amax, fabsf(ev));
+    }
+    ovf |= store_split8(eh, mat_plane(e), static_cast<long long>(r) * e.ld + c, v, inv_e);
+    store_split8(zh, mat_plane(z), static_cast<long long>(r) * z.ld + c, v, inv_e);
+  });
   if (ovf) { rmax = __uint_as_float(0x7fc00000u); amax = rmax; }
   rmax = warp_max_nonneg(rmax);
   amax = warp_max_nonneg(amax);
@@ -201,40 +194,28 @@ __global__ void cn_first_kernel(dash_stack a, const float* __restrict__ inv_scal
   int em = 0;
   if (bound_m > 0.f && bound_m < 3.0e38f) { frexpf(bound_m, &em); em -= 15; }
   const float inv_m = ldexpf(1.f, -em);
-  const __half* ah = reinterpret_cast<const __half*>(a.data) + static_cast<long long>(m) * 2 * n * a.ld;
-  const __half* al = ah + static_cast<long long>(n) * a.ld;
-  auto planes = [&](const dash_stack& s, __half*& h, __half*& l) {
-    h = reinterpret_cast<__half*>(s.data) + static_cast<long long>(m) * 2 * n * s.ld;
-    l = h + static_cast<long long>(n) * s.ld;
-  };
-  __half *xh, *xl, *mh, *ml, *ch, *cl;
-  planes(x, xh, xl);
-  planes(mm, mh, ml);
-  planes(corr, ch, cl);
+  const __half* ah = mat_hi(a, m);
+  __half* xh = mat_hi(x, m);
+  __half* mh = mat_hi(mm, m);
+  __half* ch = mat_hi(corr, m);
   float amax_m = 0.f, amax_c = 0.f;
-  const long long total = static_cast<long long>(n) * n;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int r = static_cast<int>(i / n), c = static_cast<int>(i % n);
-    const long long oa = static_cast<long long>(r) * a.ld + c;
-    const float av = (__half2float(ah[oa]) + __half2float(al[oa])) * sa;
-    const float d = (r == c) ? 1.f : 0.f;
-    const float mv = av * inv_cp;
-    const float cv = (1.f + 1.f / p) * d - mv / p;
-    const float xv = d * inv_c;
-    amax_m = nonneg_max(amax_m, fabsf(mv));
-    amax_c = nonneg_max(amax_c, fabsf(cv));
-    auto put = [&](__half* h, __half* l, int ld, float v, float inv) {
-      const long long o = static_cast<long long>(r) * ld + c;
-      const float y = v * inv;
-      const __half hh = __float2half_rn(y);
-      h[o] = hh;
-      l[o] = __float2half_rn(y - __half2float(hh));
-    };
-    put(xh, xl, x.ld, xv, inv_e);
-    put(mh, ml, mm.ld, mv, inv_m);
-    put(ch, cl, corr.ld, cv, inv_e);
-  }
+  for_chunks8(n, a.ld, [&](int r, int c) {
+    float av[8], xv[8], mv[8], cv[8];
+    load_split8(ah, mat_plane(a), static_cast<long long>(r) * a.ld + c, sa, av);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const bool in = c + i < n;
+      const float d = (r == c + i) ? 1.f : 0.f;
+      mv[i] = in ? av[i] * inv_cp : 0.f;
+      cv[i] = in ? (1.f + 1.f / p) * d - mv[i] / p : 0.f;
+      xv[i] = d * inv_c;
+      amax_m = nonneg_max(amax_m, fabsf(mv[i]));
+      amax_c = nonneg_max(amax_c, fabsf(cv[i]));
+    }
+    store_split8(xh, mat_plane(x), static_cast<long long>(r) * x.ld + c, xv, inv_e);
+    store_split8(mh, mat_plane(mm), static_cast<long long>(r) * mm.ld + c, mv, inv_m);
+    store_split8(ch, mat_plane(corr), static_cast<long long>(r) * corr.ld + c, cv, inv_e);
+  });
   amax_m = warp_max_nonneg(amax_m);
   amax_c = warp_max_nonneg(amax_c);
   if ((threadIdx.x & 31) == 0) {
@@ -283,30 +264,28 @@ __global__ void scale_stack_kernel(dash_stack src, const float* __restrict__ mul
   const float bound = __uint_as_float(src.amax[m]) * fabsf(mu);
   if (bound > 0.f && bound < 3.0e38f) { frexpf(bound, &e); e -= 15; }
   const float inv = ldexpf(1.f, -e);
-  const __half* sh = reinterpret_cast<const __half*>(src.data) + static_cast<long long>(m) * 2 * rows * src.ld;
-  const __half* sl = sh + static_cast<long long>(rows) * src.ld;
-  __half *dh = nullptr, *dl = nullptr;
-  if (has_dst) {
-    dh = reinterpret_cast<__half*>(dst.data) + static_cast<long long>(m) * 2 * rows * dst.ld;
-    dl = dh + static_cast<long long>(rows) * dst.ld;
-  }
+  const __half* sh = mat_hi(src, m);
+  __half* dh = has_dst ? mat_hi(dst, m) : nullptr;
   float amax = 0.f;
-  const long long total = static_cast<long long>(rows) * cols;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int r = static_cast<int>(i / cols), c = static_cast<int>(i % cols);
-    const long long o = static_cast<long long>(r) * src.ld + c;
-    const float v = (__half2float(sh[o]) + __half2float(sl[o])) * sc;
-    if (f_out) f_out[m * f_mat_stride + static_cast<long long>(r) * f_ld + c] = v;
-    if (has_dst) {
-      const float y = v * inv;
-      const __half h = __float2half_rn(y);
-      const long long od = static_cast<long long>(r) * dst.ld + c;
-      dh[od] = h;
-      dl[od] = __float2half_rn(y - __half2float(h));
-      amax = nonneg_max(amax, fabsf(v));
+  for_chunks8(rows, src.ld, [&](int r, int c) {
+    float v[8];
+    load_split8(sh, mat_plane(src), static_cast<long long>(r) * src.ld + c, sc, v);
+    if (f_out) {
+      float* fo = f_out + m * f_mat_stride + static_cast<long long>(r) * f_ld + c;
+      if (c + 8 <= cols && (f_ld & 3) == 0 && ((m * f_mat_stride) & 3) == 0) {
+        reinterpret_cast<float4*>(fo)[0] = make_float4(v[0], v[1], v[2], v[3]);
+        reinterpret_cast<float4*>(fo)[1] = make_float4(v[4], v[5], v[6], v[7]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) if (c + i < cols) fo[i] = v[i];
+      }
     }
-  }
+    if (has_dst) {
+      store_split8(dh, mat_plane(dst), static_cast<long long>(r) * dst.ld + c, v, inv);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) amax = nonneg_max(amax, fabsf(v[i]));
+    }
+  });
   if (has_dst) {
     amax = warp_max_nonneg(amax);
     if ((threadIdx.x & 31) == 0) atomic_max_nonneg(dst.amax + m, amax);
@@ -365,7 +344,7 @@ size_t ndb_ws_bytes(int n, int b) {  // NOLINT
 int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_out, const dash_stack& z_out,
               float tol, int max_iters, int passes, int* iters, float* resid_out, int* conv, void* ws,
               size_t ws_bytes, cudaStream_t st, int* products) {
-  const int n = a.nmat, b = a.rows;
+  const int n = a.nmat;
   Arena ar(ws, ws_bytes);
   dash_stack e, y2, z2;
   if (!arena_stack(ar, a, &e) || !arena_stack(ar, a, &y2) || !arena_stack(ar, a, &z2)) return DASH_EINVAL;
@@ -581,39 +560,28 @@ __global__ void cheb_first_kernel(dash_stack a, const float* __restrict__ inv_sc
   const int es = exp_bound(bound_s), e1 = exp_bound(2.f * fabsf(cd) * bound_s + fabsf(cd1)),
             e0 = exp_bound(fabsf(cd) > 0.f ? fabsf(cd) : 1.f);
   const float inv_s = ldexpf(1.f, -es), inv_1 = ldexpf(1.f, -e1), inv_0 = ldexpf(1.f, -e0);
-  const __half* ah = reinterpret_cast<const __half*>(a.data) + static_cast<long long>(m) * 2 * n * a.ld;
-  const __half* al = ah + static_cast<long long>(n) * a.ld;
-  auto planes = [&](const dash_stack& t, __half*& h, __half*& l) {
-    h = reinterpret_cast<__half*>(t.data) + static_cast<long long>(m) * 2 * n * t.ld;
-    l = h + static_cast<long long>(n) * t.ld;
-  };
-  __half *sh, *sl, *h1, *l1, *h0, *l0;
-  planes(s_out, sh, sl);
-  planes(bd1, h1, l1);
-  planes(bd, h0, l0);
+  const __half* ah = mat_hi(a, m);
+  __half* sh = mat_hi(s_out, m);
+  __half* h1 = mat_hi(bd1, m);
+  __half* h0 = mat_hi(bd, m);
   float ms = 0.f, m1 = 0.f;
-  const long long total = static_cast<long long>(n) * n;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int r = static_cast<int>(i / n), c = static_cast<int>(i % n);
-    const long long oa = static_cast<long long>(r) * a.ld + c;
-    const float d = (r == c) ? 1.f : 0.f;
-    const float sv = 2.f * ((__half2float(ah[oa]) + __half2float(al[oa])) * sa) - d;
-    const float b1 = 2.f * cd * sv + cd1 * d;
-    const float b0 = cd * d;
-    ms = nonneg_max(ms, fabsf(sv));
-    m1 = nonneg_max(m1, fabsf(b1));
-    auto put = [&](__half* h, __half* l, int ld, float v, float inv) {
-      const long long o = static_cast<long long>(r) * ld + c;
-      const float y = v * inv;
-      const __half hh = __float2half_rn(y);
-      h[o] = hh;
-      l[o] = __float2half_rn(y - __half2float(hh));
-    };
-    put(sh, sl, s_out.ld, sv, inv_s);
-    put(h1, l1, bd1.ld, b1, inv_1);
-    put(h0, l0, bd.ld, b0, inv_0);
-  }
+  for_chunks8(n, a.ld, [&](int r, int c) {
+    float sv[8], b1[8], b0[8];
+    load_split8(ah, mat_plane(a), static_cast<long long>(r) * a.ld + c, sa, sv);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const bool in = c + i < n;
+      const float d = (r == c + i) ? 1.f : 0.f;
+      sv[i] = in ? 2.f * sv[i] - d : 0.f;
+      b1[i] = in ? 2.f * cd * sv[i] + cd1 * d : 0.f;
+      b0[i] = cd * d;
+      ms = nonneg_max(ms, fabsf(sv[i]));
+      m1 = nonneg_max(m1, fabsf(b1[i]));
+    }
+    store_split8(sh, mat_plane(s_out), static_cast<long long>(r) * s_out.ld + c, sv, inv_s);
+    store_split8(h1, mat_plane(bd1), static_cast<long long>(r) * bd1.ld + c, b1, inv_1);
+    store_split8(h0, mat_plane(bd), static_cast<long long>(r) * bd.ld + c, b0, inv_0);
+  });
   ms = warp_max_nonneg(ms);
   m1 = warp_max_nonneg(m1);
   if ((threadIdx.x & 31) == 0) {

@@ -16,6 +16,7 @@
 #include <cooperative_groups.h>
 
 #include "engine.h"
+#include "elem.cuh"
 #include "ptx.cuh"
 #include "rng.cuh"
 
@@ -114,30 +115,54 @@ __global__ void __launch_bounds__(256) grad_split_kernel(const dash_block* __res
 // ---------------------------------------------------------------------------- preconditioner stats
 // In-place symmetrization ema <- (ema + ema^T) / 2 of an (n, d, d) stack (linalg.symmetrize), plus
 // per-block max|a| and sum(a^2) partials of a = ema + eps I (inputs of the solver split / Frobenius scale).
+// CTA p of a block walks the upper-triangle 32 x 32 tile pairs p, p + kPrepParts, ...: both tiles are read
+// coalesced into shared memory, averaged, and written back coalesced (the mirror through the transpose
+// buffer); the partial sums are per CTA and combined in a fixed order (deterministic).
 __global__ void __launch_bounds__(256) sym_kernel(float* __restrict__ ema, int d, float eps,
                                                   unsigned* __restrict__ amax, float* __restrict__ fro_part) {
+  __shared__ float t1[32][33], t2[32][33];
   __shared__ double sh[8];
   const int m = blockIdx.y, p = blockIdx.x;
   float* a = ema + static_cast<long long>(m) * d * d;
-  const long long total = static_cast<long long>(d) * d;
-  const long long per = (total + kPrepParts - 1) / kPrepParts;
-  const long long e0 = p * per, e1 = min(total, e0 + per);
+  const int nt = (d + 31) / 32, npairs = nt * (nt + 1) / 2;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   double fro = 0.0;
   float mx = 0.f;
-  for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-    const int r = static_cast<int>(e / d), c = static_cast<int>(e % d);
-    if (r < c) {
-      const long long o1 = static_cast<long long>(r) * d + c, o2 = static_cast<long long>(c) * d + r;
-      const float v = (a[o1] + a[o2]) * 0.5f;
-      a[o1] = v;
-      a[o2] = v;
-      fro += 2.0 * static_cast<double>(v) * v;
-      mx = nonneg_max(mx, fabsf(v));
-    } else if (r == c) {
-      const float v = a[static_cast<long long>(r) * d + c] + eps;
-      fro += static_cast<double>(v) * v;
-      mx = nonneg_max(mx, fabsf(v));
+  for (int tp = p; tp < npairs; tp += kPrepParts) {
+    int ti = 0, rem = tp;
+    while (rem >= nt - ti) { rem -= nt - ti; ++ti; }
+    const int tj = ti + rem;
+    const int r0 = ti * 32, c0 = tj * 32;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int y = ty + 8 * k;
+      t1[y][tx] = (r0 + y < d && c0 + tx < d) ? a[static_cast<long long>(r0 + y) * d + c0 + tx] : 0.f;
+      t2[y][tx] = (c0 + y < d && r0 + tx < d) ? a[static_cast<long long>(c0 + y) * d + r0 + tx] : 0.f;
     }
+    __syncthreads();
+    const bool diag = ti == tj;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int y = ty + 8 * k;
+      const int r = r0 + y, c = c0 + tx;
+      const float v = (t1[y][tx] + t2[tx][y]) * 0.5f;  // X[r][c] and X[c][r]
+      if (r < d && c < d) {
+        a[static_cast<long long>(r) * d + c] = v;
+        const float av = (r == c) ? v + eps : v;
+        fro += (diag ? 1.0 : 2.0) * static_cast<double>(av) * av;
+        mx = nonneg_max(mx, fabsf(av));
+      }
+    }
+    __syncthreads();
+    if (!diag) {  // mirror: row c0 + y of the lower tile = column of the averaged upper tile
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int y = ty + 8 * k;
+        const int r = c0 + y, c = r0 + tx;
+        if (r < d && c < d) a[static_cast<long long>(r) * d + c] = (t1[tx][y] + t2[y][tx]) * 0.5f;
+      }
+    }
+    __syncthreads();
   }
   const double t = block_sum_d<256>(fro, sh);
   if (threadIdx.x == 0) fro_part[m * kPrepParts + p] = static_cast<float>(t);
@@ -153,19 +178,24 @@ __global__ void __launch_bounds__(256) a_split_kernel(const float* __restrict__ 
   if (blockIdx.x == 0 && threadIdx.x == 0) st.exp[m] = e;
   const float inv = ldexpf(1.f, -e);
   const float* a = ema + static_cast<long long>(m) * d * d;
-  __half* hi = reinterpret_cast<__half*>(st.data) + static_cast<long long>(m) * 2 * d * st.ld;
-  __half* lo = hi + static_cast<long long>(d) * st.ld;
-  const long long total = static_cast<long long>(d) * st.ld;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int r = static_cast<int>(i / st.ld), c = static_cast<int>(i % st.ld);
-    float v = 0.f;
-    if (c < d) v = a[static_cast<long long>(r) * d + c] + (r == c ? eps : 0.f);
-    const float y = v * inv;
-    const __half h = __float2half_rn(y);
-    hi[i] = h;
-    lo[i] = __float2half_rn(y - __half2float(h));
-  }
+  __half* hi = mat_hi(st, m);
+  const bool vec = (d & 7) == 0;
+  for_chunks8(d, st.ld, [&](int r, int c) {
+    float v[8];
+    const float* src = a + static_cast<long long>(r) * d + c;
+    if (vec && c + 8 <= d) {
+      const float4 x0 = __ldg(reinterpret_cast<const float4*>(src));
+      const float4 x1 = __ldg(reinterpret_cast<const float4*>(src) + 1);
+      v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w; v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = c + i < d ? __ldg(src + i) : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (r == c + i) v[i] += eps;
+    store_split8(hi, mat_plane(st), static_cast<long long>(r) * st.ld + c, v, inv);
+  });
 }
 
 // Frobenius scale (shampoo.py:296): s = sqrt(sum a^2), fixed-order reduction of the partials.
