@@ -107,6 +107,8 @@ constexpr int kPairM = kTileM, kPairN = kTileN, kHalf = kTileM / 2, kHalfN = kTi
 constexpr int kNaccDefault = 4;   // accumulators per tile in split-f16 modes (env DASH_NACC = 1, 2, 4)
 constexpr int kEpiWarps = 8;     // 2 per TMEM lane quarter, 64 columns each
 constexpr int kSlots = 4;         // TMEM accumulator slots (4 x 128 columns = all 512)
+constexpr int kRing = 8;          // tile-index ring shared by the pair (dynamic scheduling)
+constexpr int kRingConsumers = 2 + 2 * 8;  // leader MMA + peer producer + epilogue warps of both CTAs
 constexpr int kThreads2 = 64 + 32 * kEpiWarps;
 
 template <int PASSES>
@@ -385,7 +387,8 @@ __device__ __forceinline__ void stage_transposed_f32(uint8_t* buf, const float (
 template <int PASSES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     dash_gemm2_kernel(const GemmJob* __restrict__ jobs, int njobs, int total_tiles,
-                      const CUtensorMap* __restrict__ maps, const int* __restrict__ gate, int nacc_in, int uniform) {
+                      const CUtensorMap* __restrict__ maps, const int* __restrict__ gate, int nacc_in, int uniform,
+                      int* __restrict__ tile_counter) {
   using C = Gemm2Cfg<PASSES>;
   const int nacc = nacc_in & 0xff;           // accumulators per tile (1, 2 or 4)
   const int xp = nacc_in >> 8;               // experiment knobs (DASH_EXP): 1 = hi plane loads only, 2 = no stores
@@ -399,12 +402,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + kSlots;
   uint64_t* sbar = tempty + kSlots;  // per epilogue warp: side-input TMA load
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbar + kEpiWarps);
+  uint64_t* tq_full = sbar + kEpiWarps;   // tile ring: index published (both CTAs' copies)
+  uint64_t* tq_empty = tq_full + kRing;   // tile ring: every consumer read it (leader's copy used)
+  int* tile_ring = reinterpret_cast<int*>(tq_empty + kRing);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_ring + kRing);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();  // 0 = leader (issues the pair MMAs)
-  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < C::kStages; ++s) {
@@ -416,6 +421,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       mbar_init(&tempty[a], 2 * kEpiWarps);   // every epilogue warp of both CTAs (leader's copy used)
     }
     for (int w = 0; w < kEpiWarps; ++w) mbar_init(&sbar[w], 1);
+    for (int i = 0; i < kRing; ++i) {
+      mbar_init(&tq_full[i], 1);
+      mbar_init(&tq_empty[i], kRingConsumers);
+    }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc2<kSlots * kPairN>(tmem_slot);
@@ -423,13 +432,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Dynamic tile scheduling: the leader's producer draws tiles from a global atomic counter (the pairs stay
+  // within a few tiles of each other, so every matrix's operands are read from HBM about once and reused
+  // from L2) and publishes them through a ring in both CTAs; -1 ends the stream.
+  const uint32_t leader_tq_empty = mapa_shared(smem_u32(tq_empty), 0);
+  auto next_tile = [&](uint32_t i) -> int {  // consumer side (one thread)
+    const uint32_t slot = i % kRing;
+    mbar_wait_cluster(&tq_full[slot], (i / kRing) & 1u);
+    const int tile = *reinterpret_cast<volatile int*>(&tile_ring[slot]);
+    mbar_arrive_remote(leader_tq_empty + slot * 8);
+    return tile;
+  };
 
   if (warp == 0) {
     // ------------------------------------------------------------------ TMA producer (both CTAs)
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = pair; tile < total_tiles; tile += npairs) {
+      const uint32_t peer_ring = mapa_shared(smem_u32(tile_ring), 1);
+      const uint32_t peer_full = mapa_shared(smem_u32(tq_full), 1);
+      for (uint32_t it = 0;; ++it) {
+        int tile;
+        if (rank == 0) {
+          const uint32_t slot = it % kRing;
+          mbar_wait_cluster(&tq_empty[slot], ((it / kRing) & 1u) ^ 1u);
+          tile = atomicAdd(tile_counter, 1);
+          if (tile >= total_tiles) {
+            tile = -1;
+            // the last pair to run dry re-arms the counters for the next launch on this stream
+            if (atomicAdd(tile_counter + 1, 1) == static_cast<int>(gridDim.x / 2) - 1) {
+              tile_counter[0] = 0;
+              tile_counter[1] = 0;
+              __threadfence();
+            }
+          }
+          tile_ring[slot] = tile;
+          st_cluster_u32(peer_ring + slot * 4, static_cast<uint32_t>(tile));
+          mbar_arrive(&tq_full[slot]);
+          mbar_arrive_remote(peer_full + slot * 8);
+        } else {
+          tile = next_tile(it);
+        }
+        if (tile < 0) break;
         const GemmJob& jb = jobs[find_job(jobs, njobs, tile, uniform)];
         int ti, tj;
         tile_coords(jb, tile - jb.tile_start, ti, tj);
@@ -470,7 +514,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t t = 0;
-      for (int tile = pair; tile < total_tiles; tile += npairs, ++t) {
+      for (;; ++t) {
+        const int tile = next_tile(t);
+        if (tile < 0) break;
         const GemmJob& jb = jobs[find_job(jobs, njobs, tile, uniform)];
         const int nk = (jb.K + kTileK - 1) / kTileK;
         const int per = (nk + nacc - 1) / nacc;  // k-blocks per accumulator slot
@@ -526,7 +572,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     uint32_t sphase = 0;
     const uint32_t leader_tempty = mapa_shared(smem_u32(tempty), 0);
     uint32_t t = 0;
-    for (int tile = pair; tile < total_tiles; tile += npairs, ++t) {
+    for (;; ++t) {
+      int tile = 0;
+      if (lane == 0) tile = next_tile(t);
+      tile = __shfl_sync(0xffffffffu, tile, 0);
+      if (tile < 0) break;
       const GemmJob& jb = jobs[find_job(jobs, njobs, tile, uniform)];
       const int local = tile - jb.tile_start;
       int ti, tj;
@@ -761,6 +811,19 @@ unsigned long long g_launches = 0;
 
 void note_launch(int n) { g_launches += static_cast<unsigned long long>(n); }
 
+// Per-stream pair of device counters (tile counter, finished pairs) for the dynamic tile scheduler; the
+// kernel re-arms them to zero when it finishes, so launches on one stream can reuse them back to back.
+static int* tile_counter_for(cudaStream_t stream) {
+  static std::vector<std::pair<cudaStream_t, int*>> table;
+  for (auto& e : table)
+    if (e.first == stream) return e.second;
+  int* p = nullptr;
+  if (cudaMalloc(&p, 2 * sizeof(int)) != cudaSuccess) return nullptr;
+  if (cudaMemset(p, 0, 2 * sizeof(int)) != cudaSuccess) return nullptr;
+  table.emplace_back(stream, p);
+  return p;
+}
+
 int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtensorMap* d_maps, int passes,
                 cudaStream_t stream, const int* gate, double flops, int uniform, double issued) {
   if (total_tiles <= 0) return 0;
@@ -803,6 +866,8 @@ int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtenso
   const int grid = total_tiles < g_num_sms ? total_tiles : g_num_sms;
   cudaError_t err;
   const int grid2 = 2 * (total_tiles < g_num_sms / 2 ? total_tiles : g_num_sms / 2);  // CTA pairs
+  int* counter = tile_counter_for(stream);
+  if (!counter) return 3;
   (void)grid;
   if (passes == 3) {
     static bool attr = false;
@@ -811,7 +876,8 @@ int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtenso
       attr = true;
     }
     dash_gemm2_kernel<3><<<grid2, kThreads2, Gemm2Cfg<3>::kSmemBytes, stream>>>(d_jobs, njobs, total_tiles, d_maps,
-                                                                                gate, g_nacc | (g_exp << 8), uniform);
+                                                                                gate, g_nacc | (g_exp << 8), uniform,
+                                                                                counter);
   } else {
     static bool attr = false;
     if (!attr) {
@@ -819,7 +885,8 @@ int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtenso
       attr = true;
     }
     dash_gemm2_kernel<1><<<grid2, kThreads2, Gemm2Cfg<1>::kSmemBytes, stream>>>(d_jobs, njobs, total_tiles, d_maps,
-                                                                                gate, 1 | (g_exp << 8), uniform);
+                                                                                gate, 1 | (g_exp << 8), uniform,
+                                                                                counter);
   }
   if (e1) cudaEventRecord(e1, stream);
   err = cudaGetLastError();
