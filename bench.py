@@ -235,15 +235,18 @@ def run_dash(args):
         h2d = sum(t.numel() * 4 for t in hp) + sum(t.numel() * 4 for t in hg)
         d2h = sum(t.numel() * 4 for t in hp)
         state_e = init_state(hp, cfg)
-        out, state_e = step(state_e, hp, hg, cfg)  # warm the host path
+        for _ in range(max(args.warmup, 2)):  # warm the host path (pinned output buffers cycle through the cache)
+            out, state_e = step(state_e, hp, hg, cfg)
+            del out
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.steps):
             out, state_e = step(state_e, hp, hg, cfg)
+            del out  # the caller keeps what it needs; the pinned block returns to the host cache
         torch.cuda.synchronize()
         e2e_ms = (time.perf_counter() - t0) / args.steps * 1e3
         e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
-        del state_e, out
+        del state_e
 
     fl = solver_flops(shapes, bsz, args.iters, args.solver)
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}

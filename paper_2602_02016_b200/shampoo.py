@@ -524,11 +524,26 @@ def step(state: ShampooState, params, grads, cfg: ShampooConfig, seed: int = 0, 
 
     mark("start")
     accumulate(state, grads, cfg)
+    host_params = isinstance(params[0], torch.Tensor) and not params[0].is_cuda and params[0].is_pinned()
+    prefetch = None
+    if host_params:  # H2D of the (pinned) parameters overlaps the refresh on a side stream
+        if len(params) != len(rt.shapes):
+            raise ValueError(f"expected {len(rt.shapes)} parameter tensors, got {len(params)}")
+        if getattr(rt, "copy_stream", None) is None:
+            rt.copy_stream = torch.cuda.Stream(device=rt.dev)
+        rt.copy_stream.wait_stream(torch.cuda.current_stream())  # after the gradient H2D + statistics
+        with torch.cuda.stream(rt.copy_stream):
+            rt.load(rt.theta, params)
+        prefetch = torch.cuda.Event()
+        prefetch.record(rt.copy_stream)
     mark("accumulated")
     refresh_inverse_roots(state, cfg, seed=block_seed(seed, t))
     mark("refreshed")
     eta = cfg.lr.value(t)
-    rt.load(rt.theta, params)
+    if prefetch is not None:
+        torch.cuda.current_stream().wait_event(prefetch)
+    else:
+        rt.load(rt.theta, params)
     _lib.check(_lib.lib().dash_plan_apply(rt.plan, rt.theta.data_ptr(), rt.theta_out.data_ptr(), float(eta),
                                           _lib.stream_ptr()), "dash_plan_apply")
     mark("applied")
