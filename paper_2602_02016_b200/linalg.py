@@ -210,3 +210,43 @@ def bmm(a, b, mode: PrecisionMode = PrecisionMode.EMULATED32, *, trans_a: bool =
 
 def symmetrize(a: torch.Tensor) -> torch.Tensor:
     return (a + a.transpose(-1, -2)) * 0.5
+
+
+# ----------------------------------------------------------------------------- text matrices (host)
+def format_matrix(a) -> str:
+    """'rows cols' header + one line of %.17g values per row (linalg.py:150-154), from a 2-D array/tensor."""
+    if isinstance(a, torch.Tensor):
+        a = a.detach().to("cpu", torch.float64).numpy()
+    a = np.asarray(a, dtype=np.float64)
+    if a.ndim != 2:
+        raise ValueError(f"format_matrix expects a 2-D array, got shape {a.shape}")
+    lines = [f"{a.shape[0]} {a.shape[1]}"]
+    lines.extend(" ".join(format(v, ".17g") for v in row) for row in a.tolist())
+    return "\n".join(lines) + "\n"
+
+
+def parse_matrix(text: str) -> np.ndarray:
+    """Inverse of format_matrix with the reference's validation (linalg.py:157-173); returns float64."""
+    lines = [ln for ln in text.splitlines() if ln.strip()]
+    if not lines:
+        raise ValueError("empty matrix text")
+    header = lines[0].split()
+    if len(header) != 2:
+        raise ValueError(f"bad matrix header: {lines[0]!r}")
+    rows, cols = int(header[0]), int(header[1])
+    if len(lines) - 1 != rows:
+        raise ValueError(f"expected {rows} data rows, got {len(lines) - 1}")
+    out = np.empty((rows, cols), dtype=np.float64)
+    for i, ln in enumerate(lines[1:]):
+        vals = ln.split()
+        if len(vals) != cols:
+            raise ValueError(f"expected {cols} values per row, got {len(vals)}")
+        out[i] = np.array(vals, dtype=np.float64)
+    if not np.isfinite(out).all():
+        raise ValueError("matrix entries must be finite")
+    return out
+
+
+def load_matrix(path) -> np.ndarray:
+    with open(path) as fh:
+        return parse_matrix(fh.read())

@@ -30,7 +30,7 @@ from .blocking import PartitionLayout, chunk_bounds, partition_layout
 from .chebyshev import ChebCoefficients, clenshaw_split, fit_inverse_root
 from .eigensolver import DampeningHeuristic, HeuristicKind, evd_inverse_root_torch
 from .errors import ConvergenceError, DegenerateSpectrumError
-from .linalg import PrecisionMode, SplitStack, device, passes_for, workspace
+from .linalg import PrecisionMode, SplitStack, device, format_matrix, parse_matrix, passes_for, workspace
 from .roots import CnConfig, DeviceReports, cn_split, ndb_split
 from .spectral import Frobenius, PowerIterationScaling, ScalingMode, block_seed, power_iteration_scales
 
@@ -562,3 +562,140 @@ def step(state: ShampooState, params, grads, cfg: ShampooConfig, seed: int = 0, 
             p_.copy_(o)
         return list(params), state
     return [o.clone() for o in outs], state
+
+
+# ============================================================================ checkpointing
+def _config_echo(cfg: ShampooConfig) -> list[str]:
+    """The reference's config echo lines (shampoo.py:409-430)."""
+    scaling = cfg.solver.scaling
+    scaling_desc = "fro" if isinstance(scaling, Frobenius) else f"pi pool={scaling.pool} iters={scaling.iters}"
+    return [
+        f"beta_lr = {cfg.beta_lr!r}",
+        f"epsilon = {cfg.epsilon!r}",
+        f"update_freq = {cfg.update_freq}",
+        f"block_size = {cfg.block_size}",
+        f"solver = {cfg.solver.method}",
+        f"scaling = {scaling_desc}",
+        f"tolerance = {cfg.solver.tolerance!r}",
+        f"max_iters = {cfg.solver.max_iters}",
+        f"precision = {cfg.solver.precision.value}",
+        f"lr_kind = {cfg.lr.kind}",
+        f"lr_base = {cfg.lr.base!r}",
+        f"graft_beta1 = {cfg.graft.beta1!r}",
+        f"graft_beta2 = {cfg.graft.beta2!r}",
+        f"graft_eps = {cfg.graft.graft_eps!r}",
+    ]
+
+
+def _block_sections(state: ShampooState):
+    """(header, group, slot) of every ema/root section in the reference's order (shampoo.py:443-454)."""
+    for layer in state.layers:
+        refs = [("L", layer.left_refs)]
+        if layer.right_refs is not None:
+            refs.append(("R", layer.right_refs))
+        for side, ref_list in refs:
+            for idx, ref in enumerate(ref_list):
+                yield layer, side, idx, ref
+
+
+def save_state(state: ShampooState, cfg: ShampooConfig, path) -> None:
+    """Single-file text checkpoint in the reference's format v1 (shampoo.py:433-461).
+
+    The device state is fp32; every value is written as the float64 of that fp32 number (%.17g), so a
+    reference process can load_state it, and our load_state reads reference checkpoints."""
+    lines = ["# blockshampoo checkpoint v1", f"step = {state.step}"]
+    lines.extend(_config_echo(cfg))
+    lines.append(f"momentum = {0 if state.momentum is None else 1}")
+    lines.append(f"layer_count = {len(state.layers)}")
+    for layer in state.layers:
+        lines.append(f"layer {layer.layer_id} shape = {' '.join(str(d) for d in layer.shape)}")
+    ema_host = [g.ema.double().cpu().numpy() for g in state.groups]  # one D2H per group
+    root_host = [g.roots.double().cpu().numpy() for g in state.groups]
+    parts = ["\n".join(lines) + "\n"]
+    last = None
+    for layer, side, idx, ref in _block_sections(state):
+        if last is not None and last is not layer:
+            parts.extend(_layer_tail(state, last))
+        last = layer
+        parts.append(f"[layer {layer.layer_id} side {side} block {idx} ema]\n")
+        parts.append(format_matrix(ema_host[ref.group][ref.slot]))
+        parts.append(f"[layer {layer.layer_id} side {side} block {idx} root]\n")
+        parts.append(format_matrix(root_host[ref.group][ref.slot]))
+    if last is not None:
+        parts.extend(_layer_tail(state, last))
+    with open(path, "w") as fh:
+        fh.write("".join(parts))
+
+
+def _layer_tail(state: ShampooState, layer: LayerState) -> list[str]:
+    out = []
+    adam = state.adam[layer.layer_id].double().cpu().numpy()
+    out.append(f"[layer {layer.layer_id} adam]\n")
+    out.append(format_matrix(adam if adam.ndim == 2 else adam[None, :]))
+    if state.momentum is not None:
+        mom = state.momentum[layer.layer_id].double().cpu().numpy()
+        out.append(f"[layer {layer.layer_id} momentum]\n")
+        out.append(format_matrix(mom if mom.ndim == 2 else mom[None, :]))
+    return out
+
+
+def load_state(path) -> tuple[ShampooState, dict[str, str]]:
+    """Rebuild a checkpointed state on the device; returns it with the echoed config (shampoo.py:464-519).
+
+    Same validation and error messages as the reference; the float64 text values are rounded to fp32."""
+    with open(path) as fh:
+        text = fh.read()
+    head, *sections = text.split("\n[")
+    meta: dict[str, str] = {}
+    shapes: dict[int, tuple[int, ...]] = {}
+    for line in head.splitlines():
+        line = line.strip()
+        if not line or line.startswith("#"):
+            continue
+        key, _, value = line.partition("=")
+        key, value = key.strip(), value.strip()
+        if key.startswith("layer ") and key.endswith(" shape"):
+            shapes[int(key.split()[1])] = tuple(int(v) for v in value.split())
+        else:
+            meta[key] = value
+    expected = int(meta["layer_count"])
+    if sorted(shapes) != list(range(expected)):
+        raise ValueError("checkpoint is missing layer shape declarations")
+    state = _build_structure([shapes[i] for i in range(expected)], int(meta["block_size"]), meta["momentum"] == "1")
+    state.step = int(meta["step"])
+    ema_host = [np.zeros(tuple(g.ema.shape), dtype=np.float32) for g in state.groups]
+    root_host = [g.roots.cpu().numpy().copy() for g in state.groups]
+    seen: set[str] = set()
+    for section in sections:
+        header, _, body = section.partition("]\n")
+        tokens = header.split()
+        layer = state.layers[int(tokens[1])]
+        data = parse_matrix(body)
+        if tokens[2] == "adam":
+            state.adam[layer.layer_id].copy_(torch.from_numpy(data if layer.is_matrix else data[0]))
+        elif tokens[2] == "momentum":
+            if state.momentum is None:
+                raise ValueError("checkpoint has momentum sections but momentum flag is 0")
+            state.momentum[layer.layer_id].copy_(torch.from_numpy(data if layer.is_matrix else data[0]))
+        else:
+            side, idx, kind = tokens[3], int(tokens[5]), tokens[6]
+            ref = (layer.left_refs if side == "L" else layer.right_refs)[idx]
+            (ema_host if kind == "ema" else root_host)[ref.group][ref.slot] = data
+        seen.add(header)
+    for layer in state.layers:
+        sides = ["L"] + (["R"] if layer.right_refs is not None else [])
+        for side in sides:
+            for idx in range(len(layer.left_refs)):
+                for kind in ("ema", "root"):
+                    key = f"layer {layer.layer_id} side {side} block {idx} {kind}"
+                    if key not in seen:
+                        raise ValueError(f"checkpoint is missing section [{key}]")
+        if f"layer {layer.layer_id} adam" not in seen:
+            raise ValueError(f"checkpoint is missing section [layer {layer.layer_id} adam]")
+    rt: _Runtime = state.runtime
+    for gi, g in enumerate(state.groups):
+        g.ema.copy_(torch.from_numpy(ema_host[gi]))
+        g.roots.copy_(torch.from_numpy(root_host[gi]))
+        rt.root_split[gi].load(g.roots)  # the apply operand (used until the next refresh)
+    torch.cuda.synchronize()
+    return state, meta

@@ -117,7 +117,30 @@ def step_fixture():
     np.savez_compressed(OUT / "steps.npz", **res)
 
 
+def checkpoint_fixture():
+    """Reference text checkpoint after 3 steps (mini set, NDB fixed, momentum on) + the 4th step's outputs."""
+    rng = np.random.default_rng(21)
+    params = [rng.standard_normal(s) for s in MINI]
+    grads_seq = [[rng.standard_normal(s) for s in MINI] for _ in range(4)]
+    cfg = shampoo.ShampooConfig(block_size=16, solver=shampoo.SolverConfig(method="ndb", tolerance=0.0, max_iters=10),
+                                graft=shampoo.GraftConfig(beta1=0.9))
+    state = shampoo.init_state(params, cfg)
+    cur = [p.copy() for p in params]
+    for gs in grads_seq[:3]:
+        cur, state = shampoo.step(state, cur, gs, cfg, seed=3)
+    shampoo.save_state(state, cfg, OUT / "ckpt_mini.txt")
+    res = {f"param3_{i}": p for i, p in enumerate(cur)}
+    res.update({f"grad3_{i}": g for i, g in enumerate(grads_seq[3])})
+    out, state = shampoo.step(state, cur, grads_seq[3], cfg, seed=3)
+    res.update({f"out4_{i}": p for i, p in enumerate(out)})
+    for gi, g in enumerate(state.groups):
+        res[f"ema4_{gi}"] = g.ema
+        res[f"root4_{gi}"] = g.roots
+    np.savez_compressed(OUT / "checkpoint.npz", **res)
+
+
 if __name__ == "__main__":
+    checkpoint_fixture()
     structure_fixture()
     seeds_fixture()
     solver_fixture()
