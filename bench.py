@@ -310,6 +310,13 @@ def run_dash(args):
     _, specs = build_layout(shapes, bsz)
     result["config"]["precond_blocks"] = {f"{g.dim}x{g.dim}/p{g.exponent}": len(g.members) for g in specs}
     result["phases_ms"] = phases
+    if world > 1:  # block sharding balance (balance.block_report): solver-cost makespan vs mean, all-gather bytes
+        from paper_2602_02016_b200.balance import block_balance, block_report
+
+        rep = block_report(opt.units, block_balance(opt.units, world))
+        result["balance"] = {"units": len(opt.units), "units_per_rank": list(rep.units_per_rank),
+                             "imbalance": round(rep.imbalance, 4),
+                             "allgather_bytes_per_rank": rep.allgather_bytes}
     if phases.get("refresh"):  # Newton-DB algorithmic FLOPs / refresh phase (includes PI, splits, rescale)
         result["solver_tflops_per_s"] = round(fl["ndb"] / world / (phases["refresh"] * 1e-3) / 1e12, 1)
     if rank == 0 and not args.no_cpu:

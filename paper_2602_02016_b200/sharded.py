@@ -21,6 +21,7 @@ import numpy as np
 import torch
 
 from . import _lib
+from .balance import block_balance, block_cost
 from .shampoo import (GroupSpec, LayerState, PrecondGroup, ShampooConfig, ShampooState, SlotRef, _Runtime,
                       accumulate, block_rows, build_layout, refresh_inverse_roots)
 from .spectral import block_seed
@@ -38,8 +39,7 @@ class Unit:
 
     @property
     def cost(self) -> int:
-        # two Newton-DB chains per inverse 4th root (2-D blocks), one per inverse square root (chunks)
-        return 2 * (self.rows ** 3 + self.cols ** 3) if self.matrix else self.rows ** 3
+        return block_cost(self.rows, self.cols, self.matrix)
 
 
 def units_of(layers: list[LayerState]) -> list[Unit]:
@@ -55,17 +55,13 @@ def units_of(layers: list[LayerState]) -> list[Unit]:
 
 
 def assign_units(units: list[Unit], world: int) -> list[list[int]]:
-    """Greedy LPT: units by (-cost, index) to the least-loaded rank, ties to the lowest rank."""
+    """Greedy LPT (balance.block_balance): units by (-cost, index) to the least-loaded rank, ties to the
+    lowest rank; returns each rank's unit indices in ascending order."""
     if world < 1:
         raise ValueError("need at least one rank")
-    order = sorted(range(len(units)), key=lambda i: (-units[i].cost, i))
-    loads = [0] * world
-    owned: list[list[int]] = [[] for _ in range(world)]
-    for i in order:
-        r = min(range(world), key=lambda w: (loads[w], w))
-        owned[r].append(i)
-        loads[r] += units[i].cost
-    return [sorted(o) for o in owned]
+    if not units:
+        return [[] for _ in range(world)]
+    return [sorted(w.layer_ids) for w in block_balance(units, world).workers]
 
 
 def local_groups(specs: list[GroupSpec], owned_keys: set[tuple[int, int]]):
