@@ -139,7 +139,25 @@ def checkpoint_fixture():
     np.savez_compressed(OUT / "checkpoint.npz", **res)
 
 
+def training_fixture():
+    """run_training rows of the reference on its three toy tasks (tasks.py:141-161)."""
+    runs = {
+        "quadratic_ndbfix": (tasks.QuadraticTask(seed=0), dict(method="ndb", tolerance=0.0, max_iters=10), 16, 1, 0.1),
+        "logreg_ndbfix_f2": (tasks.LogisticRegressionTask(seed=1), dict(method="ndb", tolerance=0.0, max_iters=10), 8, 2, 0.5),
+        "mlp_cnfix": (tasks.TinyMlpTask(seed=2), dict(method="cn", tolerance=0.0, max_iters=10), 8, 1, 0.05),
+    }
+    out = {}
+    for name, (task, kw, bsz, freq, lr) in runs.items():
+        cfg = shampoo.ShampooConfig(block_size=bsz, update_freq=freq, lr=shampoo.LrSchedule(base=lr),
+                                    solver=shampoo.SolverConfig(**kw))
+        rows, params = tasks.run_training(task, cfg, 12, seed=4)
+        out[name] = {"block_size": bsz, "update_freq": freq, "lr": lr, "solver": kw,
+                     "rows": [list(r) for r in rows]}
+    (OUT / "training.json").write_text(json.dumps(out))
+
+
 if __name__ == "__main__":
+    training_fixture()
     checkpoint_fixture()
     structure_fixture()
     seeds_fixture()

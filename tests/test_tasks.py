@@ -1,0 +1,67 @@
+"""Training harness: the toy tasks + run_training driving the B200 step.
+
+CPU: the task definitions equal the reference's bit for bit (live import where available).
+GPU: run_training rows against the reference's own rows (tests/golden/training.json).
+"""
+import json
+
+import numpy as np
+import pytest
+
+from paper_2602_02016_b200 import tasks
+from tests.conftest import GOLDEN
+
+
+def test_tasks_match_reference(reference):
+    import blockshampoo.tasks as ref
+
+    assert np.array_equal(tasks.random_spd(7, 30.0, seed=3, scale=0.5), ref.random_spd(7, 30.0, seed=3, scale=0.5))
+    for name in ("quadratic", "logreg", "mlp"):
+        ours, theirs = tasks.TASKS[name](seed=5), ref.TASKS[name](seed=5)
+        p1, p2 = ours.init_params(), theirs.init_params()
+        assert all(np.array_equal(a, b) for a, b in zip(p1, p2))
+        assert ours.loss(p1) == theirs.loss(p2)
+        g1, g2 = ours.grads(p1), theirs.grads(p2)
+        for a, b in zip(g1, g2):
+            assert np.allclose(a, b, rtol=1e-13, atol=1e-15)
+
+
+def test_task_gradients_finite_difference():
+    for name in ("quadratic", "logreg", "mlp"):
+        task = tasks.TASKS[name](seed=1) if name != "quadratic" else tasks.QuadraticTask(n=6, seed=1)
+        params = task.init_params()
+        grads = task.grads(params)
+        rng = np.random.default_rng(0)
+        for li, p in enumerate(params):
+            d = rng.standard_normal(p.shape)
+            h = 1e-6
+            plus = [q.copy() for q in params]
+            minus = [q.copy() for q in params]
+            plus[li] = p + h * d
+            minus[li] = p - h * d
+            fd = (task.loss(plus) - task.loss(minus)) / (2 * h)
+            assert abs(fd - float(np.sum(grads[li] * d))) < 1e-5 * max(1.0, abs(fd)), (name, li)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["quadratic_ndbfix", "logreg_ndbfix_f2", "mlp_cnfix"])
+def test_run_training_vs_reference(name):
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2602_02016_b200 import shampoo
+
+    g = json.loads((GOLDEN / "training.json").read_text())[name]
+    task = {"quadratic": tasks.QuadraticTask(seed=0), "logreg": tasks.LogisticRegressionTask(seed=1),
+            "mlp": tasks.TinyMlpTask(seed=2)}[name.split("_")[0]]
+    cfg = shampoo.ShampooConfig(block_size=g["block_size"], update_freq=g["update_freq"],
+                                lr=shampoo.LrSchedule(base=g["lr"]), solver=shampoo.SolverConfig(**g["solver"]))
+    rows, _ = tasks.run_training(task, cfg, len(g["rows"]), seed=4)
+    want = np.array(g["rows"])
+    got = np.array(rows)
+    assert np.array_equal(got[:, 0], want[:, 0]) and np.array_equal(got[:, 4], want[:, 4])  # steps, refresh flags
+    # first-step statistics are rank deficient (cond ~1e10 with eps = 1e-10): fp32-class roots differ from
+    # float64 there, so the trajectories agree to ~1e-2 rather than to the per-step parity bound
+    assert np.allclose(got[:, 1], want[:, 1], rtol=2e-2), (got[:, 1], want[:, 1])
+    assert np.allclose(got[:, 3], want[:, 3], rtol=5e-2), (got[:, 3], want[:, 3])
