@@ -104,10 +104,11 @@ __device__ __forceinline__ void store_split(__half* hi, long long plane, int ld,
 // 128 x 128 sub-block twice (direct and transposed) and drops the one below-diagonal sub-block of each
 // diagonal tile, so every output element has exactly one writer (deterministic).
 constexpr int kPairM = kTileM, kPairN = kTileN, kHalf = kTileM / 2, kHalfN = kTileN / 2;
-constexpr int kNaccDefault = 4;   // accumulators per tile in split-f16 modes (env DASH_NACC = 1, 2, 4)
+constexpr int kNaccDefault = 2;   // split-f16 accumulators per tile (env DASH_NACC = 1, 2 = main + correction, 4)
 constexpr int kEpiWarps = 8;     // 2 per TMEM lane quarter, 64 columns each
 constexpr int kSlots = 4;         // TMEM accumulator slots (4 x 128 columns = all 512)
 constexpr int kRing = 8;          // tile-index ring shared by the pair (dynamic scheduling)
+constexpr int kPrefetch = 4;      // k-blocks prefetched into L2 ahead of the producer
 constexpr int kRingConsumers = 2 + 2 * 8;  // leader MMA + peer producer + epilogue warps of both CTAs
 constexpr int kThreads2 = 64 + 32 * kEpiWarps;
 
@@ -391,6 +392,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                       int* __restrict__ tile_counter) {
   using C = Gemm2Cfg<PASSES>;
   const int nacc = nacc_in & 0xff;           // accumulators per tile (1, 2 or 4)
+  const bool mc = PASSES == 3 && nacc == 2;  // main (hi*hi) + correction (hi*lo + lo*hi) accumulators
   const int xp = nacc_in >> 8;               // experiment knobs (DASH_EXP): 1 = hi plane loads only, 2 = no stores
   const uint32_t nsets = kSlots / nacc;      // tiles in flight in TMEM
 
@@ -483,9 +485,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         const CUtensorMap* amap = maps + jb.a_map;
         const CUtensorMap* bmap = maps + jb.b_map;
         const int a_mn = jb.a_mn, b_mn = jb.b_mn, a_mat = jb.a_mat, b_mat = jb.b_mat;
+        // L2 prefetch kPrefetch k-blocks beyond the shared-memory ring: the ring only covers ~3 k-blocks of
+        // MMA time, less than an HBM miss, and every tile's first touch of an operand block misses L2
+        auto prefetch = [&](int kb) {
+          const int k0 = kb * kTileK;
+          for (int p = 0; p < C::kPlanes; ++p) {
+            if (!a_mn) {
+              tma_prefetch_4d(amap, k0, am, p, a_mat);
+            } else {
+              tma_prefetch_4d(amap, am, k0, p, a_mat);
+              tma_prefetch_4d(amap, am + 64, k0, p, a_mat);
+            }
+            if (!b_mn) tma_prefetch_4d(bmap, k0, bn, p, b_mat);
+            else tma_prefetch_4d(bmap, bn, k0, p, b_mat);
+          }
+        };
+        if (xp & 16)  // experiment knob: L2 prefetch ahead of the ring (measured: no gain)
+          for (int kb = 0; kb < kPrefetch && kb < nk; ++kb) prefetch(kb);
         for (int kb = 0; kb < nk; ++kb) {
+          if ((xp & 16) && kb + kPrefetch < nk) prefetch(kb + kPrefetch);
           mbar_wait(&empty[stage], phase ^ 1);
-          const int nplanes = (xp & 1) ? 1 : C::kPlanes;
+          const int nplanes = (xp & 32) ? 0 : (xp & 1) ? 1 : C::kPlanes;  // experiment knobs (no / half loads)
           if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * C::kStageBytes / C::kPlanes * nplanes);
           uint8_t* sA = smem + stage * C::kStageBytes;
           uint8_t* sB = sA + C::kABytes * C::kPlanes;
@@ -510,30 +530,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer (leader CTA only)
-    if (rank == 0 && elect_one()) {
+    // The whole warp runs the loop (warp-uniform control flow); one elected lane issues each MMA / commit.
+    if (rank == 0) {
       int stage = 0;
       uint32_t phase = 0;
       uint32_t t = 0;
       for (;; ++t) {
-        const int tile = next_tile(t);
+        int tile = 0;
+        if (lane == 0) tile = next_tile(t);
+        tile = __shfl_sync(0xffffffffu, tile, 0);
         if (tile < 0) break;
         const GemmJob& jb = jobs[find_job(jobs, njobs, tile, uniform)];
         const int nk = (jb.K + kTileK - 1) / kTileK;
-        const int per = (nk + nacc - 1) / nacc;  // k-blocks per accumulator slot
-        const uint32_t idesc = umma_idesc_f16(kPairM, kPairN, jb.a_mn, jb.b_mn);
+        // main + correction mode (nacc == 2, split products): hi*hi -> slot 0, hi*lo + lo*hi -> slot 1 over the
+        // whole K; otherwise slot c takes the k-blocks [c*per, (c+1)*per)
+        const int per = mc ? nk : (nk + nacc - 1) / nacc;
+        // experiment knob 64: issue N = 256 instructions (timing only, with knobs 2 | 32: no loads / epilogue)
+        const uint32_t idesc = umma_idesc_f16(kPairM, (xp & 64) ? 2 * kPairN : kPairN, jb.a_mn, jb.b_mn);
         const uint32_t a_lbo = jb.a_mn ? 8192u : 16u, b_lbo = jb.b_mn ? 8192u : 16u;
         const uint32_t a_kstep = jb.a_mn ? 2048u : 32u, b_kstep = jb.b_mn ? 2048u : 32u;
         const uint32_t base = (t % nsets) * static_cast<uint32_t>(nacc);
         const uint32_t use_par = ((t / nsets) & 1u) ^ 1u;
-        int c = 0;
+        int c = 0, kin = 0;  // accumulator slot, k-block index within the slot's K range
         for (int kb = 0; kb < nk; ++kb) {
-          const bool first = (kb % per) == 0;
+          const bool first = kin == 0;
           const uint32_t slot = base + static_cast<uint32_t>(c);
           if (first) {
             mbar_wait(&tempty[slot], use_par);
+            if (mc) mbar_wait(&tempty[slot + 1], use_par);
             tc_fence_after();
           }
-          const uint32_t d_tmem = tmem_base + slot * kPairN;
+          const uint32_t d_tmem = (xp & 64) ? tmem_base : tmem_base + slot * kPairN;
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_base = smem_u32(smem + stage * C::kStageBytes);
@@ -546,21 +573,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
               const uint32_t bp = (p == 1) ? 1u : 0u;  // pass 1: A_hi * B_lo
               const uint64_t ad = umma_sdesc(a_base + ap * C::kABytes + k * a_kstep, a_lbo, 1024);
               const uint64_t bd = umma_sdesc(b_base + bp * C::kBBytes + k * b_kstep, b_lbo, 1024);
-              umma2_f16(d_tmem, ad, bd, idesc, (first && k == 0 && p == 0) ? 0u : 1u);
+              // main + correction mode: passes 1, 2 go to the next slot, whose first write is pass 1
+              const uint32_t fresh = (first && k == 0 && (p == 0 || (mc && p == 1))) ? 0u : 1u;
+              umma2_f16_elect(d_tmem + ((mc && p) ? kPairN : 0u), ad, bd, idesc, fresh);
             }
           }
-          umma2_commit_mc(&empty[stage]);
+          umma2_commit_mc_elect(&empty[stage]);
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
-          if ((kb % per) == per - 1 || kb == nk - 1) {
-            umma2_commit_mc(&tfull[slot]);  // this slot's K range is complete
+          if (++kin == per || kb == nk - 1) {
+            umma2_commit_mc_elect(&tfull[slot]);  // this slot's K range is complete
             ++c;
+            if (mc) {
+              umma2_commit_mc_elect(&tfull[slot + 1]);
+              ++c;
+            }
+            kin = 0;
           }
         }
         for (; c < nacc; ++c) {  // slots without k-blocks (nk < nacc): keep every slot's phase in step
           const uint32_t slot = base + static_cast<uint32_t>(c);
           mbar_wait(&tempty[slot], use_par);
           tc_fence_after();
-          umma2_commit_mc(&tfull[slot]);
+          umma2_commit_mc_elect(&tfull[slot]);
         }
       }
     }
@@ -584,8 +618,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       const int m0 = ti * kPairM;
       const int n0 = tj * kPairN;
       const int nk = (jb.K + kTileK - 1) / kTileK;
-      const int per = (nk + nacc - 1) / nacc;
-      const int used = (nk + per - 1) / per;
+      const int per = mc ? nk : (nk + nacc - 1) / nacc;
+      const int used = mc ? 2 : (nk + per - 1) / per;
       const uint32_t base = (t % nsets) * static_cast<uint32_t>(nacc);
       const uint32_t use_par = (t / nsets) & 1u;
       const bool side_tma = jb.s_map >= 0;
