@@ -441,8 +441,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
   auto next_tile = [&](uint32_t i) -> int {  // consumer side (one thread)
     const uint32_t slot = i % kRing;
     mbar_wait_cluster(&tq_full[slot], (i / kRing) & 1u);
-    const int tile = *reinterpret_cast<volatile int*>(&tile_ring[slot]);
-    mbar_arrive_remote(leader_tq_empty + slot * 8);
+    const int tile = ld_acquire_shared(&tile_ring[slot]);  // completes before the (relaxed) release of the slot
+    mbar_arrive_remote_relaxed(leader_tq_empty + slot * 8);
     return tile;
   };
 
@@ -654,7 +654,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_remote(leader_tempty + slot * 8);
+        if (lane == 0) mbar_arrive_remote_relaxed(leader_tempty + slot * 8);
       }
       // ---- fused epilogue on the fp32 sums
       EpiCtx cx;
