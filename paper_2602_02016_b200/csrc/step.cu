@@ -444,6 +444,10 @@ __device__ void pi2_matvec(const float* __restrict__ a, int d, float eps, int ro
 #pragma unroll
     for (int u = 0; u < kPi2Ahead; ++u) pre[u] = __ldg(p + u * st4);
     const int rounds = d / (kPi2Splits * kPi2Ahead);
+    const int vstep = kPi2Splits * (kPiPool / 4);  // float4 stride of V between my consecutive k steps
+    float4 vn[kPi2Cols / 4];                        // V row of the next k step (shared loads one step ahead)
+#pragma unroll
+    for (int j4 = 0; j4 < kPi2Cols / 4; ++j4) vn[j4] = vks[j4];
     for (int rd = 0; rd < rounds; ++rd) {
       const bool more = rd + 1 < rounds;
       const float4* pn = p + static_cast<long long>(kPi2Ahead) * (rd + 1) * st4;
@@ -451,11 +455,18 @@ __device__ void pi2_matvec(const float* __restrict__ a, int d, float eps, int ro
       for (int u = 0; u < kPi2Ahead; ++u) {
         const float4 av = pre[u];
         if (more) pre[u] = __ldg(pn + u * st4);
-        const float4* vk = vks + (kPi2Ahead * rd + u) * kPi2Splits * (kPiPool / 4);
+        float4 vc[kPi2Cols / 4];
+#pragma unroll
+        for (int j4 = 0; j4 < kPi2Cols / 4; ++j4) vc[j4] = vn[j4];
+        if (more || u + 1 < kPi2Ahead) {
+          const float4* vk = vks + (kPi2Ahead * rd + u + 1) * vstep;
+#pragma unroll
+          for (int j4 = 0; j4 < kPi2Cols / 4; ++j4) vn[j4] = vk[j4];
+        }
         const float ar[4] = {av.x, av.y, av.z, av.w};
 #pragma unroll
         for (int j4 = 0; j4 < kPi2Cols / 4; ++j4) {
-          const float4 vv = vk[j4];
+          const float4 vv = vc[j4];
           const float vr[4] = {vv.x, vv.y, vv.z, vv.w};
 #pragma unroll
           for (int i = 0; i < 4; ++i)
