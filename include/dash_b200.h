@@ -139,6 +139,11 @@ int dash_group_split_a(const float* ema, float eps, const dash_stack* a, void* s
 int dash_fro_scale(const float* fro_part, int n, float* scale, float* inv_scale, void* stream);
 int dash_power_iteration(const float* ema, int n, int d, float eps, int pool, int iters, unsigned long long seed,
                          float* scale, float* inv_scale, int* status, const int* seed_index, void* stream);
+/* Same result from the solver's split stack a = ema + eps I (d a multiple of 128, <= 1024): tensor-core
+ * matvecs (tcgen05, one d/128-CTA cluster per block, pool in shared memory).  Replaces the inner loop of
+ * spectral.multi_power_iteration (spectral.py:77-112) for the DASH block sizes. */
+int dash_power_iteration_split(const dash_stack* a, int pool, int iters, unsigned long long seed, float* scale,
+                               float* inv_scale, int* status, const int* seed_index, void* stream);
 /* Block sharding exchange: copy blocks[b] (device table) of the flat space to/from the block-major
  * packed buffer at offsets pos[b] (device), around the all-gather of updated parameter shards. */
 int dash_pack_blocks(const dash_block* blocks, int n, const long long* pos, const float* flat, float* packed,

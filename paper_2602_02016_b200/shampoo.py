@@ -450,7 +450,7 @@ def refresh_inverse_roots(state: ShampooState, cfg: ShampooConfig, seed: int = 0
         else:
             power_iteration_scales(group.ema, cfg.epsilon, solver.scaling.pool, solver.scaling.iters,
                                    block_seed(seed, gids[gi] if gids is not None else gi), scale, inv, status,
-                                   sidx[gi] if sidx is not None else None)
+                                   sidx[gi] if sidx is not None else None, a_split=a)
         statuses.append((group, scale, status))
         mode = solver.precision
         if solver.method == "cbshv":

@@ -8,6 +8,8 @@ reference's ``default_rng(block_seed(seed, i)).uniform(-1, 1, (pool, n))``; the 
 """
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass
 
 import numpy as np
@@ -55,11 +57,21 @@ def block_seed(seed: int, index: int) -> int:
 
 def power_iteration_scales(ema: torch.Tensor, eps: float, pool: int, iters: int, seed: int,
                            scale: torch.Tensor, inv_scale: torch.Tensor, status: torch.Tensor,
-                           seed_index: torch.Tensor | None = None) -> None:
-    """scale[i] = 2 * lambda_PI(ema[i] + eps I) with per-block seeds block_seed(seed, i) (device)."""
+                           seed_index: torch.Tensor | None = None, a_split=None) -> None:
+    """scale[i] = 2 * lambda_PI(ema[i] + eps I) with per-block seeds block_seed(seed, i) (device).
+
+    With ``a_split`` (the solver's split stack of ema + eps I) and a block size that is a multiple of 128,
+    the matvecs run on the tensor cores (dash_power_iteration_split); otherwise the fp32 kernel reads ema."""
     if pool > MAX_POOL:
         raise ValueError(f"the B200 power iteration supports pool <= {MAX_POOL}")
     n, d = ema.shape[0], ema.shape[1]
+    if a_split is not None and d % 128 == 0 and d <= 1024 and not os.environ.get("DASH_PI_FP32"):
+        st = _lib.lib().dash_power_iteration_split(a_split.ref(), int(pool), int(iters), int(seed) & (2**64 - 1),
+                                                   scale.data_ptr(), inv_scale.data_ptr(), status.data_ptr(),
+                                                   seed_index.data_ptr() if seed_index is not None else None,
+                                                   _lib.stream_ptr())
+        _lib.check(st, "dash_power_iteration_split")
+        return
     st = _lib.lib().dash_power_iteration(ema.data_ptr(), n, d, float(eps), int(pool), int(iters),
                                          int(seed) & (2**64 - 1), scale.data_ptr(), inv_scale.data_ptr(),
                                          status.data_ptr(),

@@ -204,3 +204,25 @@ def test_c1_config_fixed_iterations_vs_oracle():
     assert relf(out[0] - w, oout[0] - w) < 2e-2
     # the update norm identity holds per block regardless of conditioning
     assert np.linalg.norm(out[0] - w) == pytest.approx(np.linalg.norm(oout[0] - w), rel=1e-4)
+
+
+@pytest.mark.parametrize("d", [128, 256, 1024])
+def test_power_iteration_tensor_cores_vs_oracle(d):
+    """Tensor-core PI (split stack of a = ema + eps I, d % 128 == 0) against the float64 oracle restatement
+    with the same per-block seeds (spectral.py:87-117): lambda within 2e-6 relative."""
+    conds = [(10.0, 0.5), (1e3, 2.0), (50.0, 1e-3)]
+    ema = np.stack([core.random_spd(d, c, seed=i, scale=s) for i, (c, s) in enumerate(conds)])
+    eps, seed = 1e-10, 777
+    et = torch.as_tensor(ema, dtype=torch.float32, device="cuda")
+    a_split = linalg.SplitStack.from_float(et + eps * torch.eye(d, device="cuda"))
+    n = ema.shape[0]
+    sc, inv = torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda")
+    st = torch.zeros(n, dtype=torch.int32, device="cuda")
+    spectral.power_iteration_scales(et, eps, 16, 30, seed, sc, inv, st, a_split=a_split)
+    sc2, inv2 = torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda")
+    spectral.power_iteration_scales(et, eps, 16, 30, seed, sc2, inv2, st)  # fp32 kernel on ema
+    want = [2.0 * core.multi_power_iteration(ema[i] + eps * np.eye(d), 16, 30, core.block_seed(seed, i))
+            for i in range(n)]
+    np.testing.assert_allclose(sc.cpu().numpy(), want, rtol=2e-6)
+    np.testing.assert_allclose(sc.cpu().numpy(), sc2.cpu().numpy(), rtol=2e-6)
+    assert int(st.abs().sum()) == 0
