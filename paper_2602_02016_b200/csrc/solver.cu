@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <initializer_list>
 #include <vector>
@@ -334,6 +335,12 @@ static void copy_stack_if(const int* par, int want, const dash_stack& dst, const
   note_launch();
 }
 
+// Every solver operand is symmetric in exact arithmetic, so B could be loaded K-major (as its transpose):
+// DASH_SYMB=1 does that.  Off by default: the 128x128 diagonal sub-blocks of the iterates are computed
+// independently and are only symmetric to rounding, and on ill-conditioned blocks the Newton iterations
+// amplify that difference (Y error 3.6e-6 -> 7.5e-5 at cond 1e3) for a 2.6% gain.
+static const int kSymB = getenv("DASH_SYMB") ? atoi(getenv("DASH_SYMB")) : 0;
+
 // ---------------------------------------------------------------------------- NDB
 size_t ndb_ws_bytes(int n, int b) {  // NOLINT
   const size_t stacks = 3 * stack_bytes(n, b, b);
@@ -359,7 +366,7 @@ int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_o
     JobBuilder jb;  // Y1 = (a E1) * inv_scale
     for (int m = 0; m < n; ++m) {
       GemmJob j;
-      if (!jb.operands(j, a, m, 0, e, m, 0)) return DASH_EINVAL;
+      if (!jb.operands(j, a, m, 0, e, m, kSymB)) return DASH_EINVAL;
       j.op = EPI_SPLIT;
       j.out_mat = m;
       j.sym = 1;
@@ -377,7 +384,7 @@ int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_o
     JobBuilder je;  // E = 1.5 I - 0.5 Z Y   (E = I for frozen blocks)
     for (int m = 0; m < n; ++m) {
       GemmJob j;
-      if (!je.operands(j, zc, m, 0, yc, m, 0)) return DASH_EINVAL;
+      if (!je.operands(j, zc, m, 0, yc, m, kSymB)) return DASH_EINVAL;
       j.op = EPI_NDB_E;
       j.out_mat = m;
       j.sym = 1;
@@ -390,13 +397,13 @@ int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_o
     JobBuilder jy;  // Y' = Y E, Z' = E Z  (reference order, roots.py:288-289)
     for (int m = 0; m < n; ++m) {
       GemmJob j;
-      if (!jy.operands(j, yc, m, 0, e, m, 0)) return DASH_EINVAL;
+      if (!jy.operands(j, yc, m, 0, e, m, kSymB)) return DASH_EINVAL;
       j.op = EPI_SPLIT;
       j.out_mat = m;
       j.sym = 1;
       jy.set_out(j, yn, m);
       jy.push(j);
-      if (!jy.operands(j, e, m, 0, zc, m, 0)) return DASH_EINVAL;
+      if (!jy.operands(j, e, m, 0, zc, m, kSymB)) return DASH_EINVAL;
       j.op = EPI_SPLIT;
       j.out_mat = m;
       j.sym = 1;
@@ -471,11 +478,11 @@ int cn_solve(const dash_stack& a, const float* inv_scale, int p, float c, const 
     JobBuilder j1;  // X' = X C and C2 = C C in one launch
     for (int m = 0; m < n; ++m) {
       GemmJob j;
-      if (!j1.operands(j, xs[par], m, 0, corr, m, 0)) return DASH_EINVAL;
+      if (!j1.operands(j, xs[par], m, 0, corr, m, kSymB)) return DASH_EINVAL;
       j.op = EPI_SPLIT; j.out_mat = m; j.sym = 1;
       j1.set_out(j, xs[par ^ 1], m);
       j1.push(j);
-      if (!j1.operands(j, corr, m, 0, corr, m, 0)) return DASH_EINVAL;
+      if (!j1.operands(j, corr, m, 0, corr, m, kSymB)) return DASH_EINVAL;
       j.op = EPI_SPLIT; j.out_mat = m; j.sym = 1;
       j1.set_out(j, cp, m);
       j1.push(j);
@@ -485,7 +492,7 @@ int cn_solve(const dash_stack& a, const float* inv_scale, int p, float c, const 
     const dash_stack& cpow = (p == 4) ? c4 : cp;
     for (int m = 0; m < n; ++m) {
       GemmJob j;
-      if (!j3.operands(j, cpow, m, 0, ms[par], m, 0)) return DASH_EINVAL;
+      if (!j3.operands(j, cpow, m, 0, ms[par], m, kSymB)) return DASH_EINVAL;
       j.op = EPI_CN_M; j.out_mat = m; j.sym = 1;
       j.beta = static_cast<float>(p);
       j.active = s.active;
@@ -500,7 +507,7 @@ int cn_solve(const dash_stack& a, const float* inv_scale, int p, float c, const 
     JobBuilder j2;
     for (int m = 0; m < n; ++m) {
       GemmJob j;
-      if (!j2.operands(j, cp, m, 0, cp, m, 0)) return DASH_EINVAL;
+      if (!j2.operands(j, cp, m, 0, cp, m, kSymB)) return DASH_EINVAL;
       j.op = EPI_SPLIT; j.out_mat = m; j.sym = 1;
       j2.set_out(j, c4, m);
       j2.push(j);
@@ -625,7 +632,7 @@ int cheb_solve(const dash_stack& a, const float* inv_scale, const float* mult, c
     JobBuilder jb;
     for (int m = 0; m < n; ++m) {
       GemmJob j;
-      if (!jb.operands(j, sm, m, 0, bb[(r + 1) % 3], m, 0)) return DASH_EINVAL;
+      if (!jb.operands(j, sm, m, 0, bb[(r + 1) % 3], m, kSymB)) return DASH_EINVAL;
       j.op = EPI_CHEB;
       j.out_mat = m;
       j.sym = 1;
@@ -640,7 +647,7 @@ int cheb_solve(const dash_stack& a, const float* inv_scale, const float* mult, c
     JobBuilder jb;
     for (int m = 0; m < n; ++m) {
       GemmJob j;
-      if (!jb.operands(j, sm, m, 0, bb[1], m, 0)) return DASH_EINVAL;
+      if (!jb.operands(j, sm, m, 0, bb[1], m, kSymB)) return DASH_EINVAL;
       j.op = EPI_CHEB_FINAL;
       j.out_mat = m;
       j.sym = 1;
