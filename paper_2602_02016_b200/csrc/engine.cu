@@ -27,7 +27,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-bool make_stack_map(const dash_stack& s, int box_rows, CUtensorMap* out, int box_cols, int box_planes, bool swz) {
+bool make_stack_map(const dash_stack& s, int box_rows, CUtensorMap* out, int box_cols, int box_planes, int swz) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[4] = {static_cast<cuuint64_t>(s.ld), static_cast<cuuint64_t>(s.rows), 2,
@@ -38,7 +38,8 @@ bool make_stack_map(const dash_stack& s, int box_rows, CUtensorMap* out, int box
                        static_cast<cuuint32_t>(box_planes), 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, s.data, dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  swz == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -152,7 +153,7 @@ int unsplit_stack(const dash_stack& s, float* dst, long long mat_stride, int dst
 }
 
 // ---------------------------------------------------------------------------- job assembly
-int JobBuilder::add_map(const dash_stack& s, int box_rows, int box_cols, int box_planes, bool swz) {
+int JobBuilder::add_map(const dash_stack& s, int box_rows, int box_cols, int box_planes, int swz) {
   for (size_t i = 0; i < map_keys.size(); ++i) {
     const MapKey& k = map_keys[i];
     if (k.data == s.data && k.box == box_rows && k.box_cols == box_cols && k.planes == box_planes && k.swz == swz &&
@@ -179,7 +180,10 @@ bool JobBuilder::operands(GemmJob& j, const dash_stack& a, int am, int trans_a, 
   j.b_mn = trans_b ? 0 : 1;  // stored K x N -> MN-major; stored N x K -> K-major
   j.a_map = add_map(a, j.a_mn ? 64 : kTileM / 2);  // each CTA of the pair: 128 rows of A, 64 rows of B
   j.b_map = add_map(b, 64);
-  if (j.a_map < 0 || j.b_map < 0) return false;
+  // K-block 32 variant (deeper pipeline): K-major boxes 32 wide with 64-byte swizzle, MN-major boxes 32 deep
+  j.a_map32 = j.a_mn ? add_map(a, 32, 64, 1, 128) : add_map(a, kTileM / 2, 32, 1, 64);
+  j.b_map32 = j.b_mn ? add_map(b, 32, 64, 1, 128) : add_map(b, 64, 32, 1, 64);
+  if (j.a_map < 0 || j.b_map < 0 || j.a_map32 < 0 || j.b_map32 < 0) return false;
   j.a_mat = am;
   j.b_mat = bm;
   j.M = M;

@@ -11,8 +11,9 @@
 
 namespace dash {
 
+// swz: 0 none, 64 = 64-byte swizzle, anything else = 128-byte swizzle
 bool make_stack_map(const dash_stack& s, int box_rows, CUtensorMap* out, int box_cols = kTileK, int box_planes = 1,
-                    bool swz = true);
+                    int swz = 128);
 bool stack_ok(const dash_stack* s);
 int job_tiles(const GemmJob& j);  // tiles the kernel runs for one job (fewer when j.sym)
 int split_stack(const float* src, long long mat_stride, int src_ld, const dash_stack& d, cudaStream_t st);
@@ -66,7 +67,7 @@ struct JobBuilder {
     const void* data;
     int box, nmat, rows, ld;
     int box_cols, planes;
-    bool swz;
+    int swz;
   };
   std::vector<CUtensorMap> maps;
   std::vector<MapKey> map_keys;
@@ -80,7 +81,7 @@ struct JobBuilder {
     jobs.clear();
     tiles = 0;
   }
-  int add_map(const dash_stack& s, int box_rows, int box_cols = kTileK, int box_planes = 1, bool swz = true);
+  int add_map(const dash_stack& s, int box_rows, int box_cols = kTileK, int box_planes = 1, int swz = 128);
   // check = false: the caller overrides M/N/K afterwards (sub-matrices of zero-padded slots)
   bool operands(GemmJob& j, const dash_stack& a, int am, int trans_a, const dash_stack& b, int bm, int trans_b,
                 bool check = true);

@@ -112,13 +112,15 @@ constexpr int kPrefetch = 4;      // k-blocks prefetched into L2 ahead of the pr
 constexpr int kRingConsumers = 2 + 2 * 8;  // leader MMA + peer producer + epilogue warps of both CTAs
 constexpr int kThreads2 = 64 + 32 * kEpiWarps;
 
-template <int PASSES>
+// KB = K-block (64: 128-byte swizzled K rows; 32: 64-byte swizzle, twice the stages in the same shared memory
+// -> more bytes in flight per unit of MMA time, i.e. more tolerance to HBM/L2 latency).
+template <int PASSES, int KB>
 struct Gemm2Cfg {
   static constexpr int kPlanes = PASSES == 3 ? 2 : 1;
-  static constexpr int kABytes = kHalf * kTileK * 2;   // 16 KB per plane (128 rows of A)
-  static constexpr int kBBytes = kHalfN * kTileK * 2;  // 8 KB per plane (64 rows of B)
+  static constexpr int kABytes = kHalf * KB * 2;    // 16 / 8 KB per plane (128 rows of A)
+  static constexpr int kBBytes = kHalfN * KB * 2;   // 8 / 4 KB per plane (64 rows of B)
   static constexpr int kStageBytes = (kABytes + kBBytes) * kPlanes;
-  static constexpr int kStages = PASSES == 3 ? 3 : 6;
+  static constexpr int kStages = (PASSES == 3 ? 3 : 6) * (64 / KB);
   static constexpr int kEpiBytes = kEpiWarps * 8192;  // per epilogue warp: 32 x 64 split tile (2 planes)
   static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 + 512;
 };
@@ -385,12 +387,12 @@ __device__ __forceinline__ void stage_transposed_f32(uint8_t* buf, const float (
   for (int j = 0; j < 64; ++j) b[j * 32] = acc[j];
 }
 
-template <int PASSES>
+template <int PASSES, int KB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     dash_gemm2_kernel(const GemmJob* __restrict__ jobs, int njobs, int total_tiles,
                       const CUtensorMap* __restrict__ maps, const int* __restrict__ gate, int nacc_in, int uniform,
                       int* __restrict__ tile_counter) {
-  using C = Gemm2Cfg<PASSES>;
+  using C = Gemm2Cfg<PASSES, KB>;
   const int nacc = nacc_in & 0xff;           // accumulators per tile (1, 2 or 4)
   const bool mc = PASSES == 3 && nacc == 2;  // main (hi*hi) + correction (hi*lo + lo*hi) accumulators
   const int xp = nacc_in >> 8;               // experiment knobs (DASH_EXP): 1 = hi plane loads only, 2 = no stores
@@ -481,14 +483,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         tile_coords(jb, tile - jb.tile_start, ti, tj);
         const int am = ti * kPairM + kHalf * static_cast<int>(rank);
         const int bn = tj * kPairN + kHalfN * static_cast<int>(rank);
-        const int nk = (jb.K + kTileK - 1) / kTileK;
-        const CUtensorMap* amap = maps + jb.a_map;
-        const CUtensorMap* bmap = maps + jb.b_map;
+        const int nk = (jb.K + KB - 1) / KB;
+        const CUtensorMap* amap = maps + (KB == 64 ? jb.a_map : jb.a_map32);
+        const CUtensorMap* bmap = maps + (KB == 64 ? jb.b_map : jb.b_map32);
         const int a_mn = jb.a_mn, b_mn = jb.b_mn, a_mat = jb.a_mat, b_mat = jb.b_mat;
         // L2 prefetch kPrefetch k-blocks beyond the shared-memory ring: the ring only covers ~3 k-blocks of
         // MMA time, less than an HBM miss, and every tile's first touch of an operand block misses L2
         auto prefetch = [&](int kb) {
-          const int k0 = kb * kTileK;
+          const int k0 = kb * KB;
           for (int p = 0; p < C::kPlanes; ++p) {
             if (!a_mn) {
               tma_prefetch_4d(amap, k0, am, p, a_mat);
@@ -509,7 +511,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
           if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * C::kStageBytes / C::kPlanes * nplanes);
           uint8_t* sA = smem + stage * C::kStageBytes;
           uint8_t* sB = sA + C::kABytes * C::kPlanes;
-          const int k0 = kb * kTileK;
+          const int k0 = kb * KB;
 #pragma unroll
           for (int p = 0; p < C::kPlanes; ++p) {
             if (p >= nplanes) break;
@@ -519,7 +521,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
               tma2_load_4d(a_dst, amap, &full[stage], k0, am, p, a_mat);
             } else {
               tma2_load_4d(a_dst, amap, &full[stage], am, k0, p, a_mat);
-              tma2_load_4d(a_dst + 8192, amap, &full[stage], am + 64, k0, p, a_mat);
+              tma2_load_4d(a_dst + 64 * KB * 2, amap, &full[stage], am + 64, k0, p, a_mat);
             }
             if (!b_mn) tma2_load_4d(b_dst, bmap, &full[stage], k0, bn, p, b_mat);
             else tma2_load_4d(b_dst, bmap, &full[stage], bn, k0, p, b_mat);
@@ -541,14 +543,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         tile = __shfl_sync(0xffffffffu, tile, 0);
         if (tile < 0) break;
         const GemmJob& jb = jobs[find_job(jobs, njobs, tile, uniform)];
-        const int nk = (jb.K + kTileK - 1) / kTileK;
+        const int nk = (jb.K + KB - 1) / KB;
         // main + correction mode (nacc == 2, split products): hi*hi -> slot 0, hi*lo + lo*hi -> slot 1 over the
         // whole K; otherwise slot c takes the k-blocks [c*per, (c+1)*per)
         const int per = mc ? nk : (nk + nacc - 1) / nacc;
         // experiment knob 64: issue N = 256 instructions (timing only, with knobs 2 | 32: no loads / epilogue)
         const uint32_t idesc = umma_idesc_f16(kPairM, (xp & 64) ? 2 * kPairN : kPairN, jb.a_mn, jb.b_mn);
-        const uint32_t a_lbo = jb.a_mn ? 8192u : 16u, b_lbo = jb.b_mn ? 8192u : 16u;
+        // K-major: 128-byte (KB 64) or 64-byte (KB 32) swizzled rows, 8-row groups 1024 / 512 B apart, 32 B per
+        // 16-wide k step; MN-major: 128-byte rows along M/N, 64-column groups KB * 128 B apart, 2 KB per k step
+        constexpr uint32_t kSbo = KB == 64 ? 1024u : 512u, kLay = KB == 64 ? 2u : 4u;
+        const uint32_t a_lbo = jb.a_mn ? KB * 128u : 16u, b_lbo = jb.b_mn ? KB * 128u : 16u;
         const uint32_t a_kstep = jb.a_mn ? 2048u : 32u, b_kstep = jb.b_mn ? 2048u : 32u;
+        const uint32_t a_sbo = jb.a_mn ? 1024u : kSbo, b_sbo = jb.b_mn ? 1024u : kSbo;
+        const uint32_t a_lay = jb.a_mn ? 2u : kLay, b_lay = jb.b_mn ? 2u : kLay;
         const uint32_t base = (t % nsets) * static_cast<uint32_t>(nacc);
         const uint32_t use_par = ((t / nsets) & 1u) ^ 1u;
         int c = 0, kin = 0;  // accumulator slot, k-block index within the slot's K range
@@ -566,13 +573,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
           const uint32_t a_base = smem_u32(smem + stage * C::kStageBytes);
           const uint32_t b_base = a_base + C::kABytes * C::kPlanes;
 #pragma unroll
-          for (int k = 0; k < kTileK / 16; ++k) {
+          for (int k = 0; k < KB / 16; ++k) {
 #pragma unroll
             for (int p = 0; p < PASSES; ++p) {
               const uint32_t ap = (p == 2) ? 1u : 0u;  // pass 2: A_lo * B_hi
               const uint32_t bp = (p == 1) ? 1u : 0u;  // pass 1: A_hi * B_lo
-              const uint64_t ad = umma_sdesc(a_base + ap * C::kABytes + k * a_kstep, a_lbo, 1024);
-              const uint64_t bd = umma_sdesc(b_base + bp * C::kBBytes + k * b_kstep, b_lbo, 1024);
+              const uint64_t ad = umma_sdesc(a_base + ap * C::kABytes + k * a_kstep, a_lbo, a_sbo, a_lay);
+              const uint64_t bd = umma_sdesc(b_base + bp * C::kBBytes + k * b_kstep, b_lbo, b_sbo, b_lay);
               // main + correction mode: passes 1, 2 go to the next slot, whose first write is pass 1
               const uint32_t fresh = (first && k == 0 && (p == 0 || (mc && p == 1))) ? 0u : 1u;
               umma2_f16_elect(d_tmem + ((mc && p) ? kPairN : 0u), ad, bd, idesc, fresh);
@@ -617,7 +624,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       tile_coords(jb, local, ti, tj);
       const int m0 = ti * kPairM;
       const int n0 = tj * kPairN;
-      const int nk = (jb.K + kTileK - 1) / kTileK;
+      const int nk = (jb.K + KB - 1) / KB;
       const int per = mc ? nk : (nk + nacc - 1) / nacc;
       const int used = mc ? 2 : (nk + per - 1) / per;
       const uint32_t base = (t % nsets) * static_cast<uint32_t>(nacc);
@@ -831,6 +838,8 @@ static int g_num_sms = 0;
 static int g_nacc = 0;
 static int g_dbg = -1;
 static int g_exp = -1;
+static int g_kb = 0;
+constexpr int kKbDefault = 64;   // K-block of the launches (env DASH_KB = 32 | 64)
 
 // Launch accounting + optional CUDA-event timing of every GEMM launch (bench / roofline hooks).
 struct GemmTimer {
@@ -844,6 +853,19 @@ static GemmTimer g_timer;
 unsigned long long g_launches = 0;
 
 void note_launch(int n) { g_launches += static_cast<unsigned long long>(n); }
+
+template <int PASSES, int KB>
+static void launch_variant(int grid2, cudaStream_t stream, const GemmJob* d_jobs, int njobs, int total_tiles,
+                           const CUtensorMap* d_maps, const int* gate, int flags, int uniform, int* counter) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(dash_gemm2_kernel<PASSES, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Gemm2Cfg<PASSES, KB>::kSmemBytes);
+    attr = true;
+  }
+  dash_gemm2_kernel<PASSES, KB><<<grid2, kThreads2, Gemm2Cfg<PASSES, KB>::kSmemBytes, stream>>>(
+      d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter);
+}
 
 // Per-stream pair of device counters (tile counter, finished pairs) for the dynamic tile scheduler; the
 // kernel re-arms them to zero when it finishes, so launches on one stream can reuse them back to back.
@@ -903,25 +925,16 @@ int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtenso
   int* counter = tile_counter_for(stream);
   if (!counter) return 3;
   (void)grid;
-  if (passes == 3) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(dash_gemm2_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, Gemm2Cfg<3>::kSmemBytes);
-      attr = true;
-    }
-    dash_gemm2_kernel<3><<<grid2, kThreads2, Gemm2Cfg<3>::kSmemBytes, stream>>>(d_jobs, njobs, total_tiles, d_maps,
-                                                                                gate, g_nacc | (g_exp << 8), uniform,
-                                                                                counter);
-  } else {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(dash_gemm2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, Gemm2Cfg<1>::kSmemBytes);
-      attr = true;
-    }
-    dash_gemm2_kernel<1><<<grid2, kThreads2, Gemm2Cfg<1>::kSmemBytes, stream>>>(d_jobs, njobs, total_tiles, d_maps,
-                                                                                gate, 1 | (g_exp << 8), uniform,
-                                                                                counter);
+  if (g_kb == 0) {
+    const char* e = getenv("DASH_KB");
+    g_kb = e ? atoi(e) : kKbDefault;
+    if (g_kb != 32 && g_kb != 64) g_kb = kKbDefault;
   }
+  const int flags = (passes == 3 ? g_nacc : 1) | (g_exp << 8);
+  if (passes == 3 && g_kb == 64) launch_variant<3, 64>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter);
+  else if (passes == 3) launch_variant<3, 32>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter);
+  else if (g_kb == 64) launch_variant<1, 64>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter);
+  else launch_variant<1, 32>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter);
   if (e1) cudaEventRecord(e1, stream);
   err = cudaGetLastError();
   return err == cudaSuccess ? 0 : 3;

@@ -115,13 +115,14 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 
 // UMMA shared-memory matrix descriptor, SWIZZLE_128B, sm_100 version bits.
 //   start: byte address in smem; lbo/sbo: byte offsets (see DESIGN.md §GEMM engine).
-__device__ __forceinline__ uint64_t umma_sdesc(uint32_t start, uint32_t lbo, uint32_t sbo) {
+//   layout: 2 = SWIZZLE_128B (default), 4 = SWIZZLE_64B.
+__device__ __forceinline__ uint64_t umma_sdesc(uint32_t start, uint32_t lbo, uint32_t sbo, uint32_t layout = 2) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((start >> 4) & 0x3FFF);
   d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
   d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
   d |= static_cast<uint64_t>(1) << 46;  // version = 1 (tcgen05)
-  d |= static_cast<uint64_t>(2) << 61;  // layout = SWIZZLE_128B
+  d |= static_cast<uint64_t>(layout) << 61;
   return d;
 }
 

@@ -43,6 +43,7 @@ enum EpiOp : int {
 struct GemmJob {
   // ---- operands (TMA maps index into the map table; mat = coordinate along the stack)
   int a_map, b_map;
+  int a_map32, b_map32;  // the same operands with 32-wide K boxes (K-block 32 kernel variant)
   int a_mat, b_mat;
   int a_mn, b_mn;
   int M, N, K;
