@@ -61,9 +61,7 @@ __global__ void __launch_bounds__(256) prep_kernel(const dash_block* __restrict_
   const long long e0 = p * per, e1 = min(total, e0 + per);
   double pn = 0.0;
   float mx = 0.f;
-  for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-    const int r = static_cast<int>(e / blk.cols), c = static_cast<int>(e % blk.cols);
-    const long long i = blk.off + static_cast<long long>(r) * blk.ld + c;
+  auto one = [&](long long i) {
     const float gv = g[i];
     const float a = beta2 * adam[i] + (1.f - beta2) * gv * gv;
     adam[i] = a;
@@ -78,6 +76,45 @@ __global__ void __launch_bounds__(256) prep_kernel(const dash_block* __restrict_
     float av = fabsf(gv);
     if (!(av <= 3.0e38f)) av = __uint_as_float(0x7fc00000u);
     mx = nonneg_max(mx, av);
+  };
+  // rows of 4-aligned 4-multiple width (every 2-D block and 1-D chunk of the DASH shapes): 16-byte accesses
+  const bool contiguous = blk.ld == blk.cols || blk.rows == 1;
+  const long long w = contiguous ? total : blk.cols;  // elements per contiguous run
+  if (w % 4 == 0 && blk.off % 4 == 0 && blk.ld % 4 == 0 && (e0 % 4 == 0) && (per % 4 == 0)) {
+    for (long long e = e0 + 4 * threadIdx.x; e < e1; e += 4 * blockDim.x) {
+      const long long r = contiguous ? 0 : e / blk.cols, c = contiguous ? e : e % blk.cols;
+      const long long i = blk.off + r * blk.ld + c;
+      const float4 g4 = *reinterpret_cast<const float4*>(g + i);
+      float4 a4 = *reinterpret_cast<const float4*>(adam + i);
+      const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
+      float av4[4] = {a4.x, a4.y, a4.z, a4.w};
+      float num[4] = {gv[0], gv[1], gv[2], gv[3]};
+      if (mom) {
+        float4 m4 = *reinterpret_cast<const float4*>(mom + i);
+        float mv[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          mv[k] = beta1 * mv[k] + (1.f - beta1) * gv[k];
+          num[k] = mv[k] * bc1_inv;
+        }
+        *reinterpret_cast<float4*>(mom + i) = make_float4(mv[0], mv[1], mv[2], mv[3]);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        av4[k] = beta2 * av4[k] + (1.f - beta2) * gv[k] * gv[k];
+        const float pv = num[k] / (geps + sqrtf(av4[k] * bc2_inv));
+        pn += static_cast<double>(pv) * pv;
+        float aa = fabsf(gv[k]);
+        if (!(aa <= 3.0e38f)) aa = __uint_as_float(0x7fc00000u);
+        mx = nonneg_max(mx, aa);
+      }
+      *reinterpret_cast<float4*>(adam + i) = make_float4(av4[0], av4[1], av4[2], av4[3]);
+    }
+  } else {
+    for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+      const int r = static_cast<int>(e / blk.cols), c = static_cast<int>(e % blk.cols);
+      one(blk.off + static_cast<long long>(r) * blk.ld + c);
+    }
   }
   const double t = block_sum_d<256>(pn, sh);
   if (threadIdx.x == 0) pn_part[b * kPrepParts + p] = static_cast<float>(t);
@@ -98,18 +135,21 @@ __global__ void __launch_bounds__(256) grad_split_kernel(const dash_block* __res
     st.amax[b] = gamax[b];
   }
   const float inv = ldexpf(1.f, -e);
-  __half* hi = reinterpret_cast<__half*>(st.data) + static_cast<long long>(b) * 2 * st.rows * st.ld;
-  __half* lo = hi + static_cast<long long>(st.rows) * st.ld;
-  const long long total = static_cast<long long>(st.rows) * st.ld;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int r = static_cast<int>(i / st.ld), c = static_cast<int>(i % st.ld);
-    float y = 0.f;
-    if (r < blk.rows && c < blk.cols) y = g[blk.off + static_cast<long long>(r) * blk.ld + c] * inv;
-    const __half h = __float2half_rn(y);
-    hi[i] = h;
-    lo[i] = __float2half_rn(y - __half2float(h));
-  }
+  __half* hi = mat_hi(st, b);
+  const bool vec = blk.cols % 8 == 0 && blk.ld % 4 == 0 && blk.off % 4 == 0;
+  for_chunks8(st.rows, st.ld, [&](int r, int c) {
+    float v[8];
+    const float* src = g + blk.off + static_cast<long long>(r) * blk.ld + c;
+    if (r < blk.rows && vec && c + 8 <= blk.cols) {
+      const float4 x0 = __ldg(reinterpret_cast<const float4*>(src));
+      const float4 x1 = __ldg(reinterpret_cast<const float4*>(src) + 1);
+      v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w; v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = (r < blk.rows && c + k < blk.cols) ? src[k] : 0.f;
+    }
+    store_split8(hi, mat_plane(st), static_cast<long long>(r) * st.ld + c, v, inv);
+  });
 }
 
 // ---------------------------------------------------------------------------- preconditioner stats
@@ -710,11 +750,24 @@ __global__ void __launch_bounds__(256) update_kernel(const dash_block* __restric
   const float* u = b < nb_m ? um + static_cast<long long>(b) * bsz * bsz : uv + static_cast<long long>(b - nb_m) * bsz;
   const int uld = b < nb_m ? bsz : 1;
   const long long total = static_cast<long long>(blk.rows) * blk.cols;
-  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int r = static_cast<int>(e / blk.cols), c = static_cast<int>(e % blk.cols);
-    const long long i = blk.off + static_cast<long long>(r) * blk.ld + c;
-    theta_out[i] = theta_in[i] - k * u[static_cast<long long>(r) * uld + c];
+  if (blk.cols % 4 == 0 && blk.ld % 4 == 0 && blk.off % 4 == 0 && uld % 4 == 0) {  // 16-byte accesses
+    const int c4n = blk.cols / 4;
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total / 4;
+         e += static_cast<long long>(gridDim.x) * blockDim.x) {
+      const int r = static_cast<int>(e / c4n), c = static_cast<int>(e % c4n) * 4;
+      const long long i = blk.off + static_cast<long long>(r) * blk.ld + c;
+      const float4 t = __ldg(reinterpret_cast<const float4*>(theta_in + i));
+      const float4 uu = __ldg(reinterpret_cast<const float4*>(u + static_cast<long long>(r) * uld + c));
+      *reinterpret_cast<float4*>(theta_out + i) = make_float4(t.x - k * uu.x, t.y - k * uu.y, t.z - k * uu.z,
+                                                              t.w - k * uu.w);
+    }
+  } else {
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<long long>(gridDim.x) * blockDim.x) {
+      const int r = static_cast<int>(e / blk.cols), c = static_cast<int>(e % blk.cols);
+      const long long i = blk.off + static_cast<long long>(r) * blk.ld + c;
+      theta_out[i] = theta_in[i] - k * u[static_cast<long long>(r) * uld + c];
+    }
   }
 }
 
