@@ -395,7 +395,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
   using C = Gemm2Cfg<PASSES, KB>;
   const int nacc = nacc_in & 0xff;           // accumulators per tile (1, 2 or 4)
   const bool mc = PASSES == 3 && nacc == 2;  // main (hi*hi) + correction (hi*lo + lo*hi) accumulators
-  const int xp = nacc_in >> 8;               // experiment knobs (DASH_EXP): 1 = hi plane loads only, 2 = no stores
+  const int xp = nacc_in >> 8;  // DASH_EXP timing knobs (results invalid): 1 hi planes only, 2 no epilogue, 4 no staging, 8 no bulk stores, 16 L2 prefetch
   const uint32_t nsets = kSlots / nacc;      // tiles in flight in TMEM
 
   if (gate && *gate == 0) return;  // uniform across the grid (and thus across each pair)
@@ -507,7 +507,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         for (int kb = 0; kb < nk; ++kb) {
           if ((xp & 16) && kb + kPrefetch < nk) prefetch(kb + kPrefetch);
           mbar_wait(&empty[stage], phase ^ 1);
-          const int nplanes = (xp & 32) ? 0 : (xp & 1) ? 1 : C::kPlanes;  // experiment knobs (no / half loads)
+          const int nplanes = (xp & 1) ? 1 : C::kPlanes;  // experiment knob: hi planes only (timing)
           if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * C::kStageBytes / C::kPlanes * nplanes);
           uint8_t* sA = smem + stage * C::kStageBytes;
           uint8_t* sB = sA + C::kABytes * C::kPlanes;
@@ -547,8 +547,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         // main + correction mode (nacc == 2, split products): hi*hi -> slot 0, hi*lo + lo*hi -> slot 1 over the
         // whole K; otherwise slot c takes the k-blocks [c*per, (c+1)*per)
         const int per = mc ? nk : (nk + nacc - 1) / nacc;
-        // experiment knob 64: issue N = 256 instructions (timing only, with knobs 2 | 32: no loads / epilogue)
-        const uint32_t idesc = umma_idesc_f16(kPairM, (xp & 64) ? 2 * kPairN : kPairN, jb.a_mn, jb.b_mn);
+        const uint32_t idesc = umma_idesc_f16(kPairM, kPairN, jb.a_mn, jb.b_mn);
         // K-major: 128-byte (KB 64) or 64-byte (KB 32) swizzled rows, 8-row groups 1024 / 512 B apart, 32 B per
         // 16-wide k step; MN-major: 128-byte rows along M/N, 64-column groups KB * 128 B apart, 2 KB per k step
         constexpr uint32_t kSbo = KB == 64 ? 1024u : 512u, kLay = KB == 64 ? 2u : 4u;
@@ -567,7 +566,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             if (mc) mbar_wait(&tempty[slot + 1], use_par);
             tc_fence_after();
           }
-          const uint32_t d_tmem = (xp & 64) ? tmem_base : tmem_base + slot * kPairN;
+          const uint32_t d_tmem = tmem_base + slot * kPairN;
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_base = smem_u32(smem + stage * C::kStageBytes);
