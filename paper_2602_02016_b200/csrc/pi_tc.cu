@@ -86,13 +86,14 @@ __device__ void pt_cluster_sum(const double (&x)[2][kPtPool], int nv, double* wp
     double t[2] = {0.0, 0.0};
     for (int s = 0; s < nv; ++s)
       for (int w = 0; w < 4; ++w) t[s] += wpart[(w * 2 + s) * kPtPool + lane];
-    for (int dst = 0; dst < C; ++dst) {
+    for (int dst = 0; dst < C; ++dst)
       for (int s = 0; s < nv; ++s) {
         const uint32_t ra = mapa_shared(smem_u32(my + (q * 2 + s) * kPtPool + lane), static_cast<uint32_t>(dst));
         asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(t[s]) : "memory");
       }
-      mbar_arrive_remote(mapa_shared(smem_u32(&red[par]), static_cast<uint32_t>(dst)));
-    }
+    asm volatile("fence.acq_rel.cluster;" ::: "memory");  // one fence for all C destinations, then relaxed arrives
+    for (int dst = 0; dst < C; ++dst)
+      mbar_arrive_remote_relaxed(mapa_shared(smem_u32(&red[par]), static_cast<uint32_t>(dst)));
   }
   mbar_wait_cluster(&red[par], (red_phase >> par) & 1u);
   red_phase ^= 1u << par;
@@ -310,9 +311,9 @@ __global__ void __launch_bounds__(kPtThreads, 1)
           pt_cluster_sum(x, 1, wpart, slots, red, par, red_phase, C, q, rw, static_cast<int>(lane), tot);  // every MMA is done
           par ^= 1;
 #pragma unroll
-          for (int j = 0; j < kPtPool; ++j) {
+          for (int j = 0; j < kPtPool; ++j) {  // 1/|w_j| in float64 (one reciprocal per column)
             const double n = sqrt(tot[0][j]);
-            v[j] = n > 0.0 ? static_cast<float>(w[j] / n) : 0.f;
+            v[j] = n > 0.0 ? static_cast<float>(static_cast<double>(w[j]) * (1.0 / n)) : 0.f;
           }
           publish();
         } else {
