@@ -338,7 +338,9 @@ static void copy_stack_if(const int* par, int want, const dash_stack& dst, const
 // Every solver operand is symmetric in exact arithmetic, so B could be loaded K-major (as its transpose):
 // DASH_SYMB=1 does that.  Off by default: the 128x128 diagonal sub-blocks of the iterates are computed
 // independently and are only symmetric to rounding, and on ill-conditioned blocks the Newton iterations
-// amplify that difference (Y error 3.6e-6 -> 7.5e-5 at cond 1e3) for a 2.6% gain.
+// amplify that difference (Y error 3.6e-6 -> 7.5e-5 at cond 1e3) for a 2.6% gain.  Making the diagonal
+// sub-blocks exactly symmetric instead (upper copied onto lower in the epilogue) was tried and is worse: a
+// cond-1e3 block then trips the divergence watch in tolerance mode (iteration 17, residual 6e-3).
 static const int kSymB = getenv("DASH_SYMB") ? atoi(getenv("DASH_SYMB")) : 0;
 
 // ---------------------------------------------------------------------------- NDB
