@@ -1,0 +1,43 @@
+"""GEMM engine variants selected by environment knobs (read once per process, so each runs in a subprocess):
+K-block 32 (64-byte swizzle, DASH_KB=32) and the accumulator layouts (DASH_NACC = 1 / 2 / 4) must all give
+fp32-class products and Newton-DB results within the parity bounds of test_gpu_parity.py."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SCRIPT = r"""
+import numpy as np, torch
+from paper_2602_02016_b200 import linalg, roots
+from paper_2602_02016_b200.linalg import PrecisionMode
+from oracle import core
+torch.manual_seed(0)
+for m, n, k, tb in ((256, 256, 256, False), (300, 700, 130, True), (1024, 1024, 1024, False)):
+    a = torch.randn(2, m, k, device="cuda"); b = torch.randn(2, n if tb else k, k if tb else n, device="cuda")
+    c = linalg.bmm(a, b, PrecisionMode.EMULATED32, trans_b=tb)
+    bd = b.double().transpose(1, 2) if tb else b.double()
+    ref = a.double() @ bd
+    err = float((c.double() - ref).norm() / ref.norm())
+    assert err < 1e-5, (m, n, k, tb, err)
+a = np.stack([core.random_spd(200, c, seed=i, scale=0.5) for i, c in enumerate([10.0, 1e3])])
+y, z, rep = roots.batched_newton_db(a, roots.NdbConfig(tolerance=0.0, max_iters=10))
+yo, zo, ro = core.batched_newton_db(a, 0.0, 10)
+for i in range(2):
+    assert np.linalg.norm(y[i] - yo[i]) / np.linalg.norm(yo[i]) < 5e-5, i
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("env", [{"DASH_KB": "32"}, {"DASH_NACC": "1"}, {"DASH_NACC": "4"}])
+def test_engine_variant(env):
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", SCRIPT], cwd=root, env={**os.environ, **env, "PYTHONPATH": root},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-2000:]
