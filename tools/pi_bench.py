@@ -2,6 +2,7 @@
 from __future__ import annotations
 
 import argparse
+import os
 import sys
 from pathlib import Path
 
@@ -39,6 +40,8 @@ def main() -> None:
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
         flops = 2.0 * args.n * args.b * args.b * 16 * (it + 1)
+        if os.environ.get("DASH_PI_EXP", "0") != "0":
+            print("section cycles (wait MMA, TMEM ld, reduce, normalise, publish):", stt[1:6].tolist())
         print(f"iters={it:3d}: {ms:8.2f} ms  {flops / ms / 1e9:7.1f} TFLOP/s (fp32 FMA)  scale[0]={float(sc[0]):.6g}")
 
 
