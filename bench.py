@@ -310,6 +310,7 @@ def run_dash(args):
     _, specs = build_layout(shapes, bsz)
     result["config"]["precond_blocks"] = {f"{g.dim}x{g.dim}/p{g.exponent}": len(g.members) for g in specs}
     result["phases_ms"] = phases
+    result["hbm_peak_gb"] = round(torch.cuda.max_memory_allocated() / 1e9, 1)  # device tensors incl. workspaces
     if world > 1:  # block sharding balance (balance.block_report): solver-cost makespan vs mean, all-gather bytes
         from paper_2602_02016_b200.balance import block_balance, block_report
 
