@@ -373,6 +373,38 @@ __device__ __forceinline__ void stage_transpose_in_place(uint8_t* buf, int lane)
   }
 }
 
+// Mirror of a staged 32 x 64 split tile written straight to global memory (DASH_EXP knob 32): every lane
+// reloads its own row from the staged buffer (read-only, concurrent with the tile's bulk store), lane pairs
+// swap one packed (hi, lo) element per column pair, each lane stores two 4-byte words of the transposed tile.
+__device__ __forceinline__ void store_mirror_from_stage(const uint8_t* buf, __half* c_hi, long long plane, int ld,
+                                                        int r0, int c0, int N, int lane) {
+  uint32_t hv[32], lv[32];
+#pragma unroll
+  for (int ch = 0; ch < 8; ++ch) {
+    const int off = lane * 128 + ((ch ^ (lane & 7)) << 4);
+    const uint4 h = *reinterpret_cast<const uint4*>(buf + off);
+    const uint4 l = *reinterpret_cast<const uint4*>(buf + 4096 + off);
+    hv[4 * ch] = h.x; hv[4 * ch + 1] = h.y; hv[4 * ch + 2] = h.z; hv[4 * ch + 3] = h.w;
+    lv[4 * ch] = l.x; lv[4 * ch + 1] = l.y; lv[4 * ch + 2] = l.z; lv[4 * ch + 3] = l.w;
+  }
+  const bool even = (lane & 1) == 0;
+  uint16_t* base = reinterpret_cast<uint16_t*>(c_hi);
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const uint32_t e0 = __byte_perm(hv[j], lv[j], 0x5410), e1 = __byte_perm(hv[j], lv[j], 0x7632);
+    const uint32_t recv = __shfl_xor_sync(0xffffffffu, even ? e1 : e0, 1);
+    const int col = c0 + 2 * j + (even ? 0 : 1);
+    const int row = r0 + (lane & ~1);
+    const uint32_t lo_e = even ? e0 : recv, hi_e = even ? recv : e1;
+    const uint32_t wh = __byte_perm(lo_e, hi_e, 0x5410), wl = __byte_perm(lo_e, hi_e, 0x7632);
+    if (col < N) {
+      uint16_t* p = base + static_cast<long long>(col) * ld + row;
+      *reinterpret_cast<uint32_t*>(p) = wh;
+      *reinterpret_cast<uint32_t*>(p + plane) = wl;
+    }
+  }
+}
+
 __device__ __forceinline__ void stage_direct_f32(uint8_t* buf, const float (&acc)[64], int lane) {
 #pragma unroll
   for (int c4 = 0; c4 < 16; ++c4)
@@ -395,7 +427,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
   using C = Gemm2Cfg<PASSES, KB>;
   const int nacc = nacc_in & 0xff;           // accumulators per tile (1, 2 or 4)
   const bool mc = PASSES == 3 && nacc == 2;  // main (hi*hi) + correction (hi*lo + lo*hi) accumulators
-  const int xp = nacc_in >> 8;  // DASH_EXP timing knobs (results invalid): 1 hi planes only, 2 no epilogue, 4 no staging, 8 no bulk stores, 16 L2 prefetch
+  const int xp = nacc_in >> 8;  // DASH_EXP knobs: timing 1 hi planes only, 2 no epilogue, 4 no staging, 8 no bulk stores, 16 L2 prefetch; 32 mirror via global stores (valid, 2-3% slower)
   const uint32_t nsets = kSlots / nacc;      // tiles in flight in TMEM
 
   if (gate && *gate == 0) return;  // uniform across the grid (and thus across each pair)
@@ -738,7 +770,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
           tma_store_4d(maps + jb.c_map, ebuf, c0, r0, 0, jb.c_mat);
           bulk_commit();
         }
-        if (cx.mirror) {
+        if (cx.mirror && (xp & 32)) {
+          store_mirror_from_stage(ebuf, jb.c_hi, jb.c_plane, jb.c_ld, r0, c0, cx.N, lr);
+        } else if (cx.mirror) {
           if (lane == 0) bulk_wait_read0();
           __syncwarp();
           stage_transpose_in_place(ebuf, lr);
@@ -766,7 +800,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             tma_store_4d(maps + jb.c2_map, ebuf, c0, r0, 0, jb.c2_mat);
             bulk_commit();
           }
-          if (cx.mirror) {
+          if (cx.mirror && (xp & 32)) {
+            store_mirror_from_stage(ebuf, jb.c2_hi, jb.c2_plane, jb.c_ld, r0, c0, cx.N, lr);
+          } else if (cx.mirror) {
             if (lane == 0) bulk_wait_read0();
             __syncwarp();
             stage_transpose_in_place(ebuf, lr);
