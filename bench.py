@@ -229,9 +229,17 @@ def run_dash(args):
 
     # ---- end-to-end through the public API with host buffers (pinned), H2D + D2H inside the region
     e2e = None
+    dev_peak = 0
     if not args.no_e2e and world == 1:
         hp = [p.cpu().pin_memory() for p in params]
         hg = [g.cpu().pin_memory() for g in grads]
+        # release the device-resident run first: two optimizer states at 953M would need ~170 GB of HBM
+        dev_peak = torch.cuda.max_memory_allocated()
+        del do_step, state
+        params.clear()
+        grads.clear()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
         h2d = sum(t.numel() * 4 for t in hp) + sum(t.numel() * 4 for t in hg)
         d2h = sum(t.numel() * 4 for t in hp)
         state_e = init_state(hp, cfg)
@@ -310,7 +318,8 @@ def run_dash(args):
     _, specs = build_layout(shapes, bsz)
     result["config"]["precond_blocks"] = {f"{g.dim}x{g.dim}/p{g.exponent}": len(g.members) for g in specs}
     result["phases_ms"] = phases
-    result["hbm_peak_gb"] = round(torch.cuda.max_memory_allocated() / 1e9, 1)  # device tensors incl. workspaces
+    # peak device memory of the device-timed run (tensors incl. workspaces; the e2e run reuses it after a release)
+    result["hbm_peak_gb"] = round((dev_peak if e2e is not None else torch.cuda.max_memory_allocated()) / 1e9, 1)
     if world > 1:  # block sharding balance (balance.block_report): solver-cost makespan vs mean, all-gather bytes
         from paper_2602_02016_b200.balance import block_balance, block_report
 
