@@ -190,6 +190,7 @@ bool JobBuilder::operands(GemmJob& j, const dash_stack& a, int am, int trans_a, 
   j.N = N;
   j.K = K;
   j.tiles_n = (N + kTileN - 1) / kTileN;
+  j.tiles_n2 = (N + 255) / 256;
   j.a_exp = a.exp + am;
   j.a_amax = a.amax + am;
   j.b_exp = b.exp + bm;
@@ -262,11 +263,12 @@ void JobBuilder::set_out2(GemmJob& j, const dash_stack& c, int cm) {
   j.c2_tmap = add_map(c, 64, 32, 2, false);
 }
 
-int job_tiles(const GemmJob& j) {
+int job_tiles(const GemmJob& j, int nt) {
   const int tm = (j.M + kTileM - 1) / kTileM;
-  if (!j.sym) return tm * j.tiles_n;
-  int n = 0;  // symmetric: column tiles J >= 2I of every 256-row tile I (see tile_coords)
-  for (int i = 0; i < tm; ++i) n += j.tiles_n - 2 * i;
+  const int tn = nt == 128 ? j.tiles_n : j.tiles_n2, step = 256 / nt;
+  if (!j.sym) return tm * tn;
+  int n = 0;  // symmetric: column tiles J >= 2I (nt 128) / J >= I (nt 256) of every 256-row tile I (tile_coords)
+  for (int i = 0; i < tm; ++i) n += tn - step * i;
   return n;
 }
 
@@ -280,6 +282,9 @@ void JobBuilder::push(GemmJob& j) {
     j.c_map = j.c_tmap = j.c2_map = j.c2_tmap = -1;
   j.tile_start = tiles;
   tiles += job_tiles(j);
+  j.tile_start2 = tiles2;
+  tiles2 += job_tiles(j, 256);
+  all_sym = all_sym && j.sym;
   jobs.push_back(j);
 }
 
@@ -305,7 +310,18 @@ bool JobBuilder::upload(Arena& ar, cudaStream_t st, UploadedGemm* out) {
   for (const GemmJob& j : jobs) out->flops += 2.0 * j.M * static_cast<double>(j.N) * j.K;
   out->uniform = uniform_tiles();
   out->issued1 = issued_per_pass();
+  out->wide = wide();
   return true;
+}
+
+GemmWide JobBuilder::wide() const {
+  GemmWide w;
+  if (jobs.empty() || !all_sym) return w;
+  w.tiles = tiles2;
+  w.uniform = uniform_tiles(256);
+  for (const GemmJob& j : jobs)
+    w.issued1 += static_cast<double>(job_tiles(j, 256)) * 2.0 * kTileM * 256 * ((j.K + kTileK - 1) / kTileK) * kTileK;
+  return w;
 }
 
 double JobBuilder::issued_per_pass() const {
@@ -315,12 +331,14 @@ double JobBuilder::issued_per_pass() const {
   return f;
 }
 
-int JobBuilder::uniform_tiles() const {
+int JobBuilder::uniform_tiles(int nt) const {
   if (jobs.empty()) return 0;
-  const int t0 = jobs.size() > 1 ? jobs[1].tile_start - jobs[0].tile_start : tiles;
+  auto start = [nt](const GemmJob& j) { return nt == 128 ? j.tile_start : j.tile_start2; };
+  const int total = nt == 128 ? tiles : tiles2;
+  const int t0 = jobs.size() > 1 ? start(jobs[1]) - start(jobs[0]) : total;
   for (size_t i = 0; i < jobs.size(); ++i) {
-    const int next = i + 1 < jobs.size() ? jobs[i + 1].tile_start : tiles;
-    if (next - jobs[i].tile_start != t0 || jobs[i].tile_start != static_cast<int>(i) * t0) return 0;
+    const int next = i + 1 < jobs.size() ? start(jobs[i + 1]) : total;
+    if (next - start(jobs[i]) != t0 || start(jobs[i]) != static_cast<int>(i) * t0) return 0;
   }
   return t0;
 }
@@ -361,8 +379,9 @@ int JobBuilder::launch(void* ws, size_t ws_bytes, int passes, cudaStream_t st) {
     return DASH_ECUDA;
   double fl = 0.0;
   for (const GemmJob& j : jobs) fl += 2.0 * j.M * static_cast<double>(j.N) * j.K;
+  const GemmWide w = wide();
   return gemm_launch(d_jobs, static_cast<int>(jobs.size()), tiles, d_maps, passes, st, nullptr, fl, uniform_tiles(),
-                     issued_per_pass() * passes);
+                     issued_per_pass() * passes, &w);
 }
 
 }  // namespace dash

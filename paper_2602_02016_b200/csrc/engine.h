@@ -15,12 +15,17 @@ namespace dash {
 bool make_stack_map(const dash_stack& s, int box_rows, CUtensorMap* out, int box_cols = kTileK, int box_planes = 1,
                     int swz = 128);
 bool stack_ok(const dash_stack* s);
-int job_tiles(const GemmJob& j);  // tiles the kernel runs for one job (fewer when j.sym)
+int job_tiles(const GemmJob& j, int nt = 128);  // tiles the kernel runs for one job (fewer when j.sym)
 int split_stack(const float* src, long long mat_stride, int src_ld, const dash_stack& d, cudaStream_t st);
 int unsplit_stack(const dash_stack& s, float* dst, long long mat_stride, int dst_ld, cudaStream_t st);
+// The same launch tiled with 256-wide pair tiles (only when every job is symmetric: no per-tile partials).
+struct GemmWide {
+  int tiles = 0, uniform = 0;
+  double issued1 = 0.0;
+};
 int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtensorMap* d_maps, int passes,
                 cudaStream_t stream, const int* gate = nullptr, double flops = 0.0, int uniform = 0,
-                double issued = 0.0);
+                double issued = 0.0, const GemmWide* wide = nullptr);
 void note_launch(int n = 1);  // count non-GEMM kernel launches
 extern unsigned long long g_launches;
 void gemm_timing_enable(int on);
@@ -35,8 +40,10 @@ struct UploadedGemm {
   int uniform = 0;     // tiles per job when all jobs have the same count (O(1) tile -> job), else 0
   double flops = 0.0;   // algorithmic: sum over jobs of 2 M N K
   double issued1 = 0.0; // tensor-core flops issued per pass (tiles x 2 x 256 x 128 x padded K)
+  GemmWide wide;        // 256-wide tiling (tiles = 0: not eligible)
   int run(int passes, cudaStream_t st, const int* gate = nullptr) const {
-    return njobs ? gemm_launch(jobs, njobs, tiles, maps, passes, st, gate, flops, uniform, issued1 * passes) : 0;
+    return njobs ? gemm_launch(jobs, njobs, tiles, maps, passes, st, gate, flops, uniform, issued1 * passes, &wide)
+                 : 0;
   }
 };
 
@@ -74,12 +81,16 @@ struct JobBuilder {
   std::vector<GemmJob> jobs;
   std::vector<uint8_t> staging;
   int tiles = 0;
+  int tiles2 = 0;        // the same jobs in 256-wide pair tiles
+  bool all_sym = true;   // every job symmetric (256-wide tiling allowed)
 
   void clear() {
     maps.clear();
     map_keys.clear();
     jobs.clear();
     tiles = 0;
+    tiles2 = 0;
+    all_sym = true;
   }
   int add_map(const dash_stack& s, int box_rows, int box_cols = kTileK, int box_planes = 1, int swz = 128);
   // check = false: the caller overrides M/N/K afterwards (sub-matrices of zero-padded slots)
@@ -94,7 +105,8 @@ struct JobBuilder {
   void push(GemmJob& j);
   static size_t bytes_for(int nmaps, int njobs);
   int launch(void* ws, size_t ws_bytes, int passes, cudaStream_t st);
-  int uniform_tiles() const;
+  int uniform_tiles(int nt = 128) const;
+  GemmWide wide() const;
   double issued_per_pass() const;
   // Upload maps + jobs into the arena (one H2D copy); the builder may be reused afterwards.
   bool upload(Arena& ar, cudaStream_t st, UploadedGemm* out);

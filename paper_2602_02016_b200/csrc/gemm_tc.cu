@@ -16,15 +16,23 @@
 
 #include "ptx.cuh"
 #include "types.h"
+#include "engine.h"
 
 namespace dash {
 
+// First global tile of a job in the NT-wide tiling (NT = 128: tile_start, NT = 256: tile_start2).
+template <int NT>
+__device__ __forceinline__ int job_tile_start(const GemmJob& j) {
+  return NT == 128 ? j.tile_start : j.tile_start2;
+}
+
+template <int NT>
 __device__ __forceinline__ int find_job(const GemmJob* __restrict__ jobs, int njobs, int tile, int uniform = 0) {
   if (uniform) return tile / uniform;  // every job has `uniform` tiles (stacked solver launches)
   int lo = 0, hi = njobs - 1;
   while (lo < hi) {
     int mid = (lo + hi + 1) >> 1;
-    if (__ldg(&jobs[mid].tile_start) <= tile) lo = mid; else hi = mid - 1;
+    if (__ldg(NT == 128 ? &jobs[mid].tile_start : &jobs[mid].tile_start2) <= tile) lo = mid; else hi = mid - 1;
   }
   return lo;
 }
@@ -114,33 +122,44 @@ constexpr int kThreads2 = 64 + 32 * kEpiWarps;
 
 // KB = K-block (64: 128-byte swizzled K rows; 32: 64-byte swizzle, twice the stages in the same shared memory
 // -> more bytes in flight per unit of MMA time, i.e. more tolerance to HBM/L2 latency).
-template <int PASSES, int KB>
+// NT = pair tile width (128 or 256).  A 256 x 256 pair tile halves the shared-memory bytes per flop (the
+// 256 x 128 tile needs ~156 B/clk of the 128 B/clk an SM's shared memory delivers for split products) at the
+// price of one accumulator per tile (2 TMEM sets of 256 columns), so it serves fp16 launches and split
+// launches that accept single-accumulator error.
+template <int PASSES, int KB, int NT = 128>
 struct Gemm2Cfg {
   static constexpr int kPlanes = PASSES == 3 ? 2 : 1;
-  static constexpr int kABytes = kHalf * KB * 2;    // 16 / 8 KB per plane (128 rows of A)
-  static constexpr int kBBytes = kHalfN * KB * 2;   // 8 / 4 KB per plane (64 rows of B)
+  static constexpr int kABytes = kHalf * KB * 2;         // 16 / 8 KB per plane (128 rows of A)
+  static constexpr int kBBytes = (NT / 2) * KB * 2;      // 8 / 4 KB per plane per 64 rows of B (NT / 2 rows)
   static constexpr int kStageBytes = (kABytes + kBBytes) * kPlanes;
-  static constexpr int kStages = (PASSES == 3 ? 3 : 6) * (64 / KB);
   static constexpr int kEpiBytes = kEpiWarps * 8192;  // per epilogue warp: 32 x 64 split tile (2 planes)
+  // NT = 256: as many stages as the 227 KB of shared memory holds
+  static constexpr int kStages = NT == 128 ? (PASSES == 3 ? 3 : 6) * (64 / KB)
+                                           : (232448 - kEpiBytes - 1024 - 512) / kStageBytes;
   static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 + 512;
+  static_assert(kSmemBytes <= 232448, "shared memory per CTA");
+  static_assert((2 * kStages + 2 * kSlots + kEpiWarps + 2 * kRing) * 8 + kRing * 4 + 4 <= 512, "barrier block");
 };
 
-// Tile `local` of a job -> (256-row tile ti, 128-column tile tj).  Symmetric jobs enumerate, per row tile
-// I, only the column tiles J >= 2I.
+// Tile `local` of a job -> (256-row tile ti, NT-column tile tj).  Symmetric jobs enumerate, per row tile
+// I, only the column tiles that reach the diagonal: J >= 2I (NT = 128) or J >= I (NT = 256).
+template <int NT>
 __device__ __forceinline__ void tile_coords(const GemmJob& jb, int local, int& ti, int& tj) {
+  constexpr int step = 256 / NT;
+  const int tn = NT == 128 ? jb.tiles_n : jb.tiles_n2;
   if (!jb.sym) {
-    ti = local / jb.tiles_n;
-    tj = local - ti * jb.tiles_n;
+    ti = local / tn;
+    tj = local - ti * tn;
     return;
   }
-  int i = 0, row = jb.tiles_n;
+  int i = 0, row = tn;
   while (local >= row) {
     local -= row;
     ++i;
-    row -= 2;
+    row -= step;
   }
   ti = i;
-  tj = 2 * i + local;
+  tj = step * i + local;
 }
 
 // Transposed store of 32 values of row r (cols c0..c0+31) into rows c0.. of column r (symmetric mirror).
@@ -419,16 +438,19 @@ __device__ __forceinline__ void stage_transposed_f32(uint8_t* buf, const float (
   for (int j = 0; j < 64; ++j) b[j * 32] = acc[j];
 }
 
-template <int PASSES, int KB>
+template <int PASSES, int KB, int NT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     dash_gemm2_kernel(const GemmJob* __restrict__ jobs, int njobs, int total_tiles,
                       const CUtensorMap* __restrict__ maps, const int* __restrict__ gate, int nacc_in, int uniform,
                       int* __restrict__ tile_counter) {
-  using C = Gemm2Cfg<PASSES, KB>;
-  const int nacc = nacc_in & 0xff;           // accumulators per tile (1, 2 or 4)
+  using C = Gemm2Cfg<PASSES, KB, NT>;
+  constexpr int kPN = NT;                    // pair tile columns = TMEM columns per accumulator slot
+  constexpr int kRounds = NT / 128;          // epilogue passes over a tile (128 columns each)
+  constexpr uint32_t kSl = 512 / NT;         // TMEM slots
+  const int nacc = NT == 128 ? (nacc_in & 0xff) : 1;  // accumulators per tile (1, 2 or 4; 1 for NT = 256)
   const bool mc = PASSES == 3 && nacc == 2;  // main (hi*hi) + correction (hi*lo + lo*hi) accumulators
   const int xp = nacc_in >> 8;  // DASH_EXP knobs: timing 1 hi planes only, 2 no epilogue, 4 no staging, 8 no bulk stores, 16 L2 prefetch; 32 mirror via global stores (valid, 2-3% slower)
-  const uint32_t nsets = kSlots / nacc;      // tiles in flight in TMEM
+  const uint32_t nsets = kSl / nacc;         // tiles in flight in TMEM
 
   if (gate && *gate == 0) return;  // uniform across the grid (and thus across each pair)
   extern __shared__ uint8_t smem_raw[];
@@ -463,7 +485,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc2<kSlots * kPairN>(tmem_slot);
+  if (warp == 1) tmem_alloc2<512>(tmem_slot);
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
@@ -510,11 +532,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
           tile = next_tile(it);
         }
         if (tile < 0) break;
-        const GemmJob& jb = jobs[find_job(jobs, njobs, tile, uniform)];
+        const GemmJob& jb = jobs[find_job<NT>(jobs, njobs, tile, uniform)];
         int ti, tj;
-        tile_coords(jb, tile - jb.tile_start, ti, tj);
+        tile_coords<NT>(jb, tile - job_tile_start<NT>(jb), ti, tj);
         const int am = ti * kPairM + kHalf * static_cast<int>(rank);
-        const int bn = tj * kPairN + kHalfN * static_cast<int>(rank);
+        const int bn = tj * kPN + (kPN / 2) * static_cast<int>(rank);
         const int nk = (jb.K + KB - 1) / KB;
         const CUtensorMap* amap = maps + (KB == 64 ? jb.a_map : jb.a_map32);
         const CUtensorMap* bmap = maps + (KB == 64 ? jb.b_map : jb.b_map32);
@@ -530,8 +552,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
               tma_prefetch_4d(amap, am, k0, p, a_mat);
               tma_prefetch_4d(amap, am + 64, k0, p, a_mat);
             }
-            if (!b_mn) tma_prefetch_4d(bmap, k0, bn, p, b_mat);
-            else tma_prefetch_4d(bmap, bn, k0, p, b_mat);
+            for (int h = 0; h < NT / 128; ++h) {
+              if (!b_mn) tma_prefetch_4d(bmap, k0, bn + 64 * h, p, b_mat);
+              else tma_prefetch_4d(bmap, bn + 64 * h, k0, p, b_mat);
+            }
           }
         };
         if (xp & 16)  // experiment knob: L2 prefetch ahead of the ring (measured: no gain)
@@ -555,8 +579,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
               tma2_load_4d(a_dst, amap, &full[stage], am, k0, p, a_mat);
               tma2_load_4d(a_dst + 64 * KB * 2, amap, &full[stage], am + 64, k0, p, a_mat);
             }
-            if (!b_mn) tma2_load_4d(b_dst, bmap, &full[stage], k0, bn, p, b_mat);
-            else tma2_load_4d(b_dst, bmap, &full[stage], bn, k0, p, b_mat);
+            // B: NT / 2 rows per CTA as 64-row boxes (K-major: consecutive 8-row groups; MN-major: 64-column
+            // groups KB * 128 B apart, the LBO of the descriptor)
+#pragma unroll
+            for (int h = 0; h < NT / 128; ++h) {
+              if (!b_mn) tma2_load_4d(b_dst + h * 64 * KB * 2, bmap, &full[stage], k0, bn + 64 * h, p, b_mat);
+              else tma2_load_4d(b_dst + h * 64 * KB * 2, bmap, &full[stage], bn + 64 * h, k0, p, b_mat);
+            }
           }
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
@@ -574,12 +603,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         if (lane == 0) tile = next_tile(t);
         tile = __shfl_sync(0xffffffffu, tile, 0);
         if (tile < 0) break;
-        const GemmJob& jb = jobs[find_job(jobs, njobs, tile, uniform)];
+        const GemmJob& jb = jobs[find_job<NT>(jobs, njobs, tile, uniform)];
         const int nk = (jb.K + KB - 1) / KB;
         // main + correction mode (nacc == 2, split products): hi*hi -> slot 0, hi*lo + lo*hi -> slot 1 over the
         // whole K; otherwise slot c takes the k-blocks [c*per, (c+1)*per)
         const int per = mc ? nk : (nk + nacc - 1) / nacc;
-        const uint32_t idesc = umma_idesc_f16(kPairM, kPairN, jb.a_mn, jb.b_mn);
+        const uint32_t idesc = umma_idesc_f16(kPairM, kPN, jb.a_mn, jb.b_mn);
         // K-major: 128-byte (KB 64) or 64-byte (KB 32) swizzled rows, 8-row groups 1024 / 512 B apart, 32 B per
         // 16-wide k step; MN-major: 128-byte rows along M/N, 64-column groups KB * 128 B apart, 2 KB per k step
         constexpr uint32_t kSbo = KB == 64 ? 1024u : 512u, kLay = KB == 64 ? 2u : 4u;
@@ -598,7 +627,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             if (mc) mbar_wait(&tempty[slot + 1], use_par);
             tc_fence_after();
           }
-          const uint32_t d_tmem = tmem_base + slot * kPairN;
+          const uint32_t d_tmem = tmem_base + slot * kPN;
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_base = smem_u32(smem + stage * C::kStageBytes);
@@ -613,7 +642,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
               const uint64_t bd = umma_sdesc(b_base + bp * C::kBBytes + k * b_kstep, b_lbo, b_sbo, b_lay);
               // main + correction mode: passes 1, 2 go to the next slot, whose first write is pass 1
               const uint32_t fresh = (first && k == 0 && (p == 0 || (mc && p == 1))) ? 0u : 1u;
-              umma2_f16_elect(d_tmem + ((mc && p) ? kPairN : 0u), ad, bd, idesc, fresh);
+              umma2_f16_elect(d_tmem + ((mc && p) ? static_cast<uint32_t>(kPN) : 0u), ad, bd, idesc, fresh);
             }
           }
           umma2_commit_mc_elect(&empty[stage]);
@@ -649,159 +678,136 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       if (lane == 0) tile = next_tile(t);
       tile = __shfl_sync(0xffffffffu, tile, 0);
       if (tile < 0) break;
-      const GemmJob& jb = jobs[find_job(jobs, njobs, tile, uniform)];
-      const int local = tile - jb.tile_start;
+      const GemmJob& jb = jobs[find_job<NT>(jobs, njobs, tile, uniform)];
+      const int local = tile - job_tile_start<NT>(jb);
       int ti, tj;
-      tile_coords(jb, local, ti, tj);
+      tile_coords<NT>(jb, local, ti, tj);
       const int m0 = ti * kPairM;
-      const int n0 = tj * kPairN;
-      const int nk = (jb.K + KB - 1) / KB;
-      const int per = mc ? nk : (nk + nacc - 1) / nacc;
-      const int used = mc ? 2 : (nk + per - 1) / per;
-      const uint32_t base = (t % nsets) * static_cast<uint32_t>(nacc);
-      const uint32_t use_par = (t / nsets) & 1u;
-      const bool side_tma = jb.s_map >= 0;
-      const bool f_tma = jb.f_map >= 0;
-      const bool fin_tma = f_tma && jb.op == EPI_EMA;
-      __syncwarp();                 // every lane is done with the previous tile's staging buffer
-      if ((side_tma || fin_tma) && lane == 0) {  // stage the side / fp32 input tile while the MMAs run
-        bulk_wait_read0();          // the previous tile's bulk stores have read the buffer
-        mbar_arrive_expect_tx(&sbar[warp - 2], 8192);
-        const int tc0 = n0 + 64 * hc, tr0 = m0 + kHalf * static_cast<int>(rank) + 32 * q;
-        if (side_tma) {
-          tma_load_4d(ebuf, maps + jb.s_map, &sbar[warp - 2], tc0, tr0, 0, jb.s_mat);
-        } else {
-          tma_load_3d(ebuf, maps + jb.f_map, &sbar[warp - 2], tc0, tr0, jb.f_mat);
-          tma_load_3d(ebuf + 4096, maps + jb.f_map, &sbar[warp - 2], tc0 + 32, tr0, jb.f_mat);
-        }
-      }
-      float acc[64];
-      for (int c = 0; c < nacc; ++c) {
-        const uint32_t slot = base + static_cast<uint32_t>(c);
-        mbar_wait(&tfull[slot], use_par);
-        tc_fence_after();
-        if (c < used) {
-          const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + slot * kPairN + 64 * hc;
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            float v[32];
-            tmem_ld32(taddr + 32 * j, v);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) acc[32 * j + i] = (c == 0) ? v[i] : acc[32 * j + i] + v[i];
+      // NT = 256: two rounds over 128-column halves; TMEM is released after the last one
+      for (int rd = 0; rd < kRounds; ++rd) {
+        const int n0 = tj * kPN + 128 * rd;
+        const int nk = (jb.K + KB - 1) / KB;
+        const int per = mc ? nk : (nk + nacc - 1) / nacc;
+        const int used = mc ? 2 : (nk + per - 1) / per;
+        const uint32_t base = (t % nsets) * static_cast<uint32_t>(nacc);
+        const uint32_t use_par = (t / nsets) & 1u;
+        const bool side_tma = jb.s_map >= 0;
+        const bool f_tma = jb.f_map >= 0;
+        const bool fin_tma = f_tma && jb.op == EPI_EMA;
+        __syncwarp();                 // every lane is done with the previous tile's staging buffer
+        if ((side_tma || fin_tma) && lane == 0) {  // stage the side / fp32 input tile while the MMAs run
+          bulk_wait_read0();          // the previous tile's bulk stores have read the buffer
+          mbar_arrive_expect_tx(&sbar[warp - 2], 8192);
+          const int tc0 = n0 + 64 * hc, tr0 = m0 + kHalf * static_cast<int>(rank) + 32 * q;
+          if (side_tma) {
+            tma_load_4d(ebuf, maps + jb.s_map, &sbar[warp - 2], tc0, tr0, 0, jb.s_mat);
+          } else {
+            tma_load_3d(ebuf, maps + jb.f_map, &sbar[warp - 2], tc0, tr0, jb.f_mat);
+            tma_load_3d(ebuf + 4096, maps + jb.f_map, &sbar[warp - 2], tc0 + 32, tr0, jb.f_mat);
           }
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_remote_relaxed(leader_tempty + slot * 8);
-      }
-      // ---- fused epilogue on the fp32 sums
-      EpiCtx cx;
-      cx.op = jb.op;
-      cx.mat = jb.out_mat;
-      cx.r = m0 + kHalf * static_cast<int>(rank) + q * 32 + static_cast<int>(lane);
-      cx.M = jb.M;
-      cx.N = jb.N;
-      // symmetric job: this CTA's 128 x 128 sub-block (row block 2 ti + rank, column block tj)
-      const int rb = 2 * ti + static_cast<int>(rank);
-      cx.store = !jb.sym || rb <= tj;
-      cx.mirror = jb.sym && rb < tj;
-      cx.row_ok = cx.r < jb.M && cx.store;
-      const int ea = jb.a_exp ? __ldg(jb.a_exp) : 0;
-      const int eb = jb.b_exp ? __ldg(jb.b_exp) : 0;
-      cx.sc = ldexpf(1.f, ea + eb);
-      cx.mul = jb.alpha * (jb.alpha_p ? __ldg(jb.alpha_p + cx.mat) : 1.f);
-      cx.inactive = jb.active && __ldg(jb.active + cx.mat) == 0;
-      cx.gam = jb.gamma_p ? *jb.gamma_p : jb.gamma;
-      const float prod_bound = static_cast<float>(jb.K) * amax_of(jb.a_amax) * amax_of(jb.b_amax);
-      cx.side_scale = jb.s_hi ? ldexpf(1.f, __ldg(jb.s_exp)) : 0.f;
-      int e_out = 0;
-      switch (cx.op) {
-        case EPI_SPLIT: e_out = exp_from_bound(prod_bound * fabsf(cx.mul)); break;
-        case EPI_NDB_E: e_out = kEExp; break;
-        case EPI_CHEB: e_out = exp_from_bound(2.f * prod_bound + amax_of(jb.s_amax) + fabsf(cx.gam)); break;
-        case EPI_CHEB_FINAL:
-          e_out = exp_from_bound((prod_bound + amax_of(jb.s_amax) + fabsf(cx.gam)) * fabsf(cx.mul));
-          break;
-        case EPI_CN_M: e_out = exp_from_bound(prod_bound); break;
-        default: break;
-      }
-      if (m0 == 0 && n0 == 0 && rank == 0 && threadIdx.x == 64) {
-        if (jb.c_exp) *jb.c_exp = e_out;
-        if (jb.c2_exp) *jb.c2_exp = kEExp;
-      }
-      cx.inv_out = ldexpf(1.f, -e_out);
-      cx.inv_e = ldexpf(1.f, -kEExp);
-      cx.cn_a = 1.f + 1.f / jb.beta;
-      cx.cn_b = 1.f / jb.beta;
-      cx.amax = cx.amax2 = cx.resid = 0.f;
-      cx.sumsq = 0.0;
-      cx.ovf = cx.ovf2 = false;
-      const bool tma_out = jb.c_map >= 0;
-      cx.sbuf = nullptr;
-      cx.fbuf = nullptr;
-      cx.f_tma = f_tma;
-      cx.lane = static_cast<int>(lane);
-      cx.lc0 = n0 + 64 * hc;
-      if (side_tma || fin_tma) {
-        mbar_wait(&sbar[warp - 2], sphase);
-        sphase ^= 1u;
-        if (side_tma) cx.sbuf = ebuf;
-        else cx.fbuf = ebuf;
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int c0 = n0 + 64 * hc + 16 * j;
-        float (&v)[16] = *reinterpret_cast<float(*)[16]>(&acc[16 * j]);  // in place: final values stay in acc
-        if (c0 < jb.N && !(xp & 2)) epi_piece<16>(jb, cx, c0, v, !tma_out);
-      }
-      if ((tma_out || f_tma) && cx.store && !(xp & 2)) {
-        // ---- staged bulk-tensor stores of the split output(s), direct and (symmetric jobs) mirrored
-        const int r0 = m0 + kHalf * static_cast<int>(rank) + 32 * q;
-        const int c0 = n0 + 64 * hc;
-        const int lr = static_cast<int>(lane);
-        auto ident = [](float v, int) { return v; };
-        if (tma_out) {
-        if (lane == 0) bulk_wait_read0();  // this warp's previous stores have read the buffer
-        __syncwarp();                      // (and every lane is done with the staged side input)
-        if (!(xp & 4)) stage_direct(ebuf, acc, lr, c0, cx.inv_out, ident, cx.ovf);
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0 && !(xp & 8)) {
-          tma_store_4d(maps + jb.c_map, ebuf, c0, r0, 0, jb.c_mat);
-          bulk_commit();
-        }
-        if (cx.mirror && (xp & 32)) {
-          store_mirror_from_stage(ebuf, jb.c_hi, jb.c_plane, jb.c_ld, r0, c0, cx.N, lr);
-        } else if (cx.mirror) {
-          if (lane == 0) bulk_wait_read0();
-          __syncwarp();
-          stage_transpose_in_place(ebuf, lr);
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_4d(maps + jb.c_tmap, ebuf, r0, c0, 0, jb.c_mat);
-            bulk_commit();
+        float acc[64];
+        for (int c = 0; c < nacc; ++c) {
+          const uint32_t slot = base + static_cast<uint32_t>(c);
+          if (rd == 0) {
+            mbar_wait(&tfull[slot], use_par);
+            tc_fence_after();
+          }
+          if (c < used) {
+            const uint32_t taddr =
+                tmem_base + (static_cast<uint32_t>(q * 32) << 16) + slot * kPN + 128 * rd + 64 * hc;
+  #pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              float v[32];
+              tmem_ld32(taddr + 32 * j, v);
+  #pragma unroll
+              for (int i = 0; i < 32; ++i) acc[32 * j + i] = (c == 0) ? v[i] : acc[32 * j + i] + v[i];
+            }
+          }
+          if (rd == kRounds - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote_relaxed(leader_tempty + slot * 8);
           }
         }
-        if (jb.c2_map >= 0) {  // EPI_CN_M: next correction C = (1 + 1/p) I - M / p (I when frozen)
-          const int r = cx.r;
-          const float ca = cx.cn_a, cb = cx.cn_b;
-          const bool inact = cx.inactive;
-          auto corr = [r, ca, cb, inact](float m, int col) {
-            const float d = (r == col) ? 1.f : 0.f;
-            return inact ? d : ca * d - cb * m;
-          };
-          if (lane == 0) bulk_wait_read0();
-          __syncwarp();
-          stage_direct(ebuf, acc, lr, c0, cx.inv_e, corr, cx.ovf2);
+        // ---- fused epilogue on the fp32 sums
+        EpiCtx cx;
+        cx.op = jb.op;
+        cx.mat = jb.out_mat;
+        cx.r = m0 + kHalf * static_cast<int>(rank) + q * 32 + static_cast<int>(lane);
+        cx.M = jb.M;
+        cx.N = jb.N;
+        // symmetric job: this CTA's 128 x 128 sub-block (row block 2 ti + rank, column block n0 / 128)
+        const int rb = 2 * ti + static_cast<int>(rank), cb = n0 / 128;
+        cx.store = !jb.sym || rb <= cb;
+        cx.mirror = jb.sym && rb < cb;
+        cx.row_ok = cx.r < jb.M && cx.store;
+        const int ea = jb.a_exp ? __ldg(jb.a_exp) : 0;
+        const int eb = jb.b_exp ? __ldg(jb.b_exp) : 0;
+        cx.sc = ldexpf(1.f, ea + eb);
+        cx.mul = jb.alpha * (jb.alpha_p ? __ldg(jb.alpha_p + cx.mat) : 1.f);
+        cx.inactive = jb.active && __ldg(jb.active + cx.mat) == 0;
+        cx.gam = jb.gamma_p ? *jb.gamma_p : jb.gamma;
+        const float prod_bound = static_cast<float>(jb.K) * amax_of(jb.a_amax) * amax_of(jb.b_amax);
+        cx.side_scale = jb.s_hi ? ldexpf(1.f, __ldg(jb.s_exp)) : 0.f;
+        int e_out = 0;
+        switch (cx.op) {
+          case EPI_SPLIT: e_out = exp_from_bound(prod_bound * fabsf(cx.mul)); break;
+          case EPI_NDB_E: e_out = kEExp; break;
+          case EPI_CHEB: e_out = exp_from_bound(2.f * prod_bound + amax_of(jb.s_amax) + fabsf(cx.gam)); break;
+          case EPI_CHEB_FINAL:
+            e_out = exp_from_bound((prod_bound + amax_of(jb.s_amax) + fabsf(cx.gam)) * fabsf(cx.mul));
+            break;
+          case EPI_CN_M: e_out = exp_from_bound(prod_bound); break;
+          default: break;
+        }
+        if (m0 == 0 && n0 == 0 && rank == 0 && threadIdx.x == 64) {
+          if (jb.c_exp) *jb.c_exp = e_out;
+          if (jb.c2_exp) *jb.c2_exp = kEExp;
+        }
+        cx.inv_out = ldexpf(1.f, -e_out);
+        cx.inv_e = ldexpf(1.f, -kEExp);
+        cx.cn_a = 1.f + 1.f / jb.beta;
+        cx.cn_b = 1.f / jb.beta;
+        cx.amax = cx.amax2 = cx.resid = 0.f;
+        cx.sumsq = 0.0;
+        cx.ovf = cx.ovf2 = false;
+        const bool tma_out = jb.c_map >= 0;
+        cx.sbuf = nullptr;
+        cx.fbuf = nullptr;
+        cx.f_tma = f_tma;
+        cx.lane = static_cast<int>(lane);
+        cx.lc0 = n0 + 64 * hc;
+        if (side_tma || fin_tma) {
+          mbar_wait(&sbar[warp - 2], sphase);
+          sphase ^= 1u;
+          if (side_tma) cx.sbuf = ebuf;
+          else cx.fbuf = ebuf;
+        }
+  #pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int c0 = n0 + 64 * hc + 16 * j;
+          float (&v)[16] = *reinterpret_cast<float(*)[16]>(&acc[16 * j]);  // in place: final values stay in acc
+          if (c0 < jb.N && !(xp & 2)) epi_piece<16>(jb, cx, c0, v, !tma_out);
+        }
+        if ((tma_out || f_tma) && cx.store && !(xp & 2)) {
+          // ---- staged bulk-tensor stores of the split output(s), direct and (symmetric jobs) mirrored
+          const int r0 = m0 + kHalf * static_cast<int>(rank) + 32 * q;
+          const int c0 = n0 + 64 * hc;
+          const int lr = static_cast<int>(lane);
+          auto ident = [](float v, int) { return v; };
+          if (tma_out) {
+          if (lane == 0) bulk_wait_read0();  // this warp's previous stores have read the buffer
+          __syncwarp();                      // (and every lane is done with the staged side input)
+          if (!(xp & 4)) stage_direct(ebuf, acc, lr, c0, cx.inv_out, ident, cx.ovf);
           fence_proxy_async_smem();
           __syncwarp();
-          if (lane == 0) {
-            tma_store_4d(maps + jb.c2_map, ebuf, c0, r0, 0, jb.c2_mat);
+          if (lane == 0 && !(xp & 8)) {
+            tma_store_4d(maps + jb.c_map, ebuf, c0, r0, 0, jb.c_mat);
             bulk_commit();
           }
           if (cx.mirror && (xp & 32)) {
-            store_mirror_from_stage(ebuf, jb.c2_hi, jb.c2_plane, jb.c_ld, r0, c0, cx.N, lr);
+            store_mirror_from_stage(ebuf, jb.c_hi, jb.c_plane, jb.c_ld, r0, c0, cx.N, lr);
           } else if (cx.mirror) {
             if (lane == 0) bulk_wait_read0();
             __syncwarp();
@@ -809,54 +815,85 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_4d(maps + jb.c2_tmap, ebuf, r0, c0, 0, jb.c2_mat);
+              tma_store_4d(maps + jb.c_tmap, ebuf, r0, c0, 0, jb.c_mat);
               bulk_commit();
             }
           }
-        }
-        }  // tma_out
-        if (f_tma) {  // fp32 output: direct tile (two swizzled 32 x 32 boxes) and, if symmetric, its mirror
-          if (lane == 0) bulk_wait_read0();
-          __syncwarp();
-          stage_direct_f32(ebuf, acc, lr);
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_3d(maps + jb.f_map, ebuf, c0, r0, jb.f_mat);
-            tma_store_3d(maps + jb.f_map, ebuf + 4096, c0 + 32, r0, jb.f_mat);
-            bulk_commit();
-          }
-          if (cx.mirror) {
+          if (jb.c2_map >= 0) {  // EPI_CN_M: next correction C = (1 + 1/p) I - M / p (I when frozen)
+            const int r = cx.r;
+            const float ca = cx.cn_a, cb = cx.cn_b;
+            const bool inact = cx.inactive;
+            auto corr = [r, ca, cb, inact](float m, int col) {
+              const float d = (r == col) ? 1.f : 0.f;
+              return inact ? d : ca * d - cb * m;
+            };
             if (lane == 0) bulk_wait_read0();
             __syncwarp();
-            stage_transposed_f32(ebuf, acc, lr);
+            stage_direct(ebuf, acc, lr, c0, cx.inv_e, corr, cx.ovf2);
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_3d(maps + jb.f_tmap, ebuf, r0, c0, jb.f_mat);
+              tma_store_4d(maps + jb.c2_map, ebuf, c0, r0, 0, jb.c2_mat);
               bulk_commit();
+            }
+            if (cx.mirror && (xp & 32)) {
+              store_mirror_from_stage(ebuf, jb.c2_hi, jb.c2_plane, jb.c_ld, r0, c0, cx.N, lr);
+            } else if (cx.mirror) {
+              if (lane == 0) bulk_wait_read0();
+              __syncwarp();
+              stage_transpose_in_place(ebuf, lr);
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_4d(maps + jb.c2_tmap, ebuf, r0, c0, 0, jb.c2_mat);
+                bulk_commit();
+              }
+            }
+          }
+          }  // tma_out
+          if (f_tma) {  // fp32 output: direct tile (two swizzled 32 x 32 boxes) and, if symmetric, its mirror
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+            stage_direct_f32(ebuf, acc, lr);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_3d(maps + jb.f_map, ebuf, c0, r0, jb.f_mat);
+              tma_store_3d(maps + jb.f_map, ebuf + 4096, c0 + 32, r0, jb.f_mat);
+              bulk_commit();
+            }
+            if (cx.mirror) {
+              if (lane == 0) bulk_wait_read0();
+              __syncwarp();
+              stage_transposed_f32(ebuf, acc, lr);
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_3d(maps + jb.f_tmap, ebuf, r0, c0, jb.f_mat);
+                bulk_commit();
+              }
             }
           }
         }
-      }
-      // per-matrix reductions (max is order independent -> deterministic)
-      float am = cx.ovf ? __uint_as_float(0x7fc00000u) : cx.amax;
-      float am2 = cx.ovf2 ? __uint_as_float(0x7fc00000u) : cx.amax2;
-      float rs = cx.resid;
-      am = warp_max_nonneg(am);
-      am2 = warp_max_nonneg(am2);
-      rs = warp_max_nonneg(rs);
-      if (lane == 0 && cx.store) {
-        if (jb.c_amax) atomic_max_nonneg(jb.c_amax, am);
-        if (jb.c2_amax) atomic_max_nonneg(jb.c2_amax, am2);
-        if (jb.resid && !cx.inactive)
-          atomic_max_nonneg(jb.resid + cx.mat, (cx.op == EPI_NDB_E || cx.op == EPI_CN_M) && cx.ovf
-                                                   ? __uint_as_float(0x7fc00000u) : rs);
-      }
-      if (cx.op == EPI_APPLY) {
-        const double sacc = warp_sum_d(cx.sumsq);
-        if (lane == 0) jb.partial[local * kPartialsPerTile + rank * 8 + hc * 4 + q] = static_cast<float>(sacc);
-      }
+        // per-matrix reductions (max is order independent -> deterministic)
+        float am = cx.ovf ? __uint_as_float(0x7fc00000u) : cx.amax;
+        float am2 = cx.ovf2 ? __uint_as_float(0x7fc00000u) : cx.amax2;
+        float rs = cx.resid;
+        am = warp_max_nonneg(am);
+        am2 = warp_max_nonneg(am2);
+        rs = warp_max_nonneg(rs);
+        if (lane == 0 && cx.store) {
+          if (jb.c_amax) atomic_max_nonneg(jb.c_amax, am);
+          if (jb.c2_amax) atomic_max_nonneg(jb.c2_amax, am2);
+          if (jb.resid && !cx.inactive)
+            atomic_max_nonneg(jb.resid + cx.mat, (cx.op == EPI_NDB_E || cx.op == EPI_CN_M) && cx.ovf
+                                                     ? __uint_as_float(0x7fc00000u) : rs);
+        }
+        if (cx.op == EPI_APPLY) {  // (never in NT = 256 launches: the host keeps them to symmetric jobs)
+          const double sacc = warp_sum_d(cx.sumsq);
+          if (lane == 0) jb.partial[local * kPartialsPerTile + rank * 8 + hc * 4 + q] = static_cast<float>(sacc);
+        }
+      }  // round
     }
     if (lane == 0) bulk_wait0();  // bulk stores complete before the CTA retires
   }
@@ -864,7 +901,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
   cluster_sync_all();  // no CTA of the pair may exit while its peer still uses its TMEM / barriers
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc2<kSlots * kPairN>(tmem_base);
+    tmem_dealloc2<512>(tmem_base);
   }
 }
 
@@ -875,6 +912,7 @@ static int g_dbg = -1;
 static int g_exp = -1;
 static int g_kb = 0;
 constexpr int kKbDefault = 64;   // K-block of the launches (env DASH_KB = 32 | 64)
+constexpr int kWideDefault = 1;  // 256-wide tiles for fp16 launches of symmetric jobs (env DASH_NT)
 
 // Launch accounting + optional CUDA-event timing of every GEMM launch (bench / roofline hooks).
 struct GemmTimer {
@@ -889,16 +927,16 @@ unsigned long long g_launches = 0;
 
 void note_launch(int n) { g_launches += static_cast<unsigned long long>(n); }
 
-template <int PASSES, int KB>
+template <int PASSES, int KB, int NT = 128>
 static void launch_variant(int grid2, cudaStream_t stream, const GemmJob* d_jobs, int njobs, int total_tiles,
                            const CUtensorMap* d_maps, const int* gate, int flags, int uniform, int* counter) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(dash_gemm2_kernel<PASSES, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         Gemm2Cfg<PASSES, KB>::kSmemBytes);
+    cudaFuncSetAttribute(dash_gemm2_kernel<PASSES, KB, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Gemm2Cfg<PASSES, KB, NT>::kSmemBytes);
     attr = true;
   }
-  dash_gemm2_kernel<PASSES, KB><<<grid2, kThreads2, Gemm2Cfg<PASSES, KB>::kSmemBytes, stream>>>(
+  dash_gemm2_kernel<PASSES, KB, NT><<<grid2, kThreads2, Gemm2Cfg<PASSES, KB, NT>::kSmemBytes, stream>>>(
       d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter);
 }
 
@@ -915,9 +953,27 @@ static int* tile_counter_for(cudaStream_t stream) {
   return p;
 }
 
+// 256-wide pair tiles (DASH_NT): 0 never, 1 fp16 launches (default), 2 fp16 and split launches
+static int wide_mode() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = getenv("DASH_NT");
+    m = !e ? kWideDefault : atoi(e) == 128 ? 0 : atoi(e) == 256 ? 1 : atoi(e) == 2562 ? 2 : kWideDefault;
+  }
+  return m;
+}
+
 int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtensorMap* d_maps, int passes,
-                cudaStream_t stream, const int* gate, double flops, int uniform, double issued) {
+                cudaStream_t stream, const int* gate, double flops, int uniform, double issued,
+                const GemmWide* wide) {
   if (total_tiles <= 0) return 0;
+  const int wm = wide_mode();
+  const bool use_wide = wide && wide->tiles > 0 && (passes == 1 ? wm >= 1 : wm >= 2);
+  if (use_wide) {
+    total_tiles = wide->tiles;
+    uniform = wide->uniform;
+    issued = wide->issued1 * passes;
+  }
   ++g_launches;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (g_timer.on) {
@@ -966,7 +1022,11 @@ int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtenso
     if (g_kb != 32 && g_kb != 64) g_kb = kKbDefault;
   }
   const int flags = (passes == 3 ? g_nacc : 1) | (g_exp << 8);
-  if (passes == 3 && g_kb == 64) launch_variant<3, 64>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter);
+  if (use_wide && passes == 3 && g_kb == 64) launch_variant<3, 64, 256>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter);
+  else if (use_wide && passes == 3) launch_variant<3, 32, 256>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter);
+  else if (use_wide && g_kb == 64) launch_variant<1, 64, 256>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter);
+  else if (use_wide) launch_variant<1, 32, 256>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter);
+  else if (passes == 3 && g_kb == 64) launch_variant<3, 64>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter);
   else if (passes == 3) launch_variant<3, 32>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter);
   else if (g_kb == 64) launch_variant<1, 64>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter);
   else launch_variant<1, 32>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter);

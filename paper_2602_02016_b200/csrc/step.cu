@@ -823,6 +823,7 @@ static void set_dims(GemmJob& j, int M, int N, int K) {
   j.N = N;
   j.K = K;
   j.tiles_n = (N + kTileN - 1) / kTileN;
+  j.tiles_n2 = (N + 255) / 256;
 }
 
 static dash_stack slot_stack(const dash_stack& s) { return s; }

@@ -49,6 +49,7 @@ struct GemmJob {
   int M, N, K;
   int tiles_n;  // ceil(N / kTileN)
   int tile_start;  // first global tile index of this job
+  int tiles_n2, tile_start2;  // the same for 256-wide pair tiles (launches of symmetric jobs only)
   int op;
   int out_mat;     // index into per-matrix epilogue arrays (resid, active, alpha_p)
   int c_ld;        // split output leading dim

@@ -1,6 +1,8 @@
 """GEMM engine variants selected by environment knobs (read once per process, so each runs in a subprocess):
-K-block 32 (64-byte swizzle, DASH_KB=32) and the accumulator layouts (DASH_NACC = 1 / 2 / 4) must all give
-fp32-class products and Newton-DB results within the parity bounds of test_gpu_parity.py."""
+K-block 32 (64-byte swizzle, DASH_KB=32), the accumulator layouts (DASH_NACC = 1 / 2 / 4) and 256-wide pair
+tiles for split launches (DASH_NT=2562) must all give fp32-class products and Newton-DB results within the
+parity bounds of test_gpu_parity.py.  fp16-mode solves run with 256-wide tiles by default and with 128-wide
+tiles under DASH_NT=128; both stay within the fp16 bound."""
 import os
 import subprocess
 import sys
@@ -22,22 +24,53 @@ for m, n, k, tb in ((256, 256, 256, False), (300, 700, 130, True), (1024, 1024, 
     ref = a.double() @ bd
     err = float((c.double() - ref).norm() / ref.norm())
     assert err < 1e-5, (m, n, k, tb, err)
-a = np.stack([core.random_spd(200, c, seed=i, scale=0.5) for i, c in enumerate([10.0, 1e3])])
-y, z, rep = roots.batched_newton_db(a, roots.NdbConfig(tolerance=0.0, max_iters=10))
-yo, zo, ro = core.batched_newton_db(a, 0.0, 10)
-for i in range(2):
-    assert np.linalg.norm(y[i] - yo[i]) / np.linalg.norm(yo[i]) < 5e-5, i
+for b in (200, 384):  # 384: two row tiles, a ragged last column tile in both tilings
+    a = np.stack([core.random_spd(b, c, seed=i, scale=0.5) for i, c in enumerate([10.0, 1e3])])
+    y, z, rep = roots.batched_newton_db(a, roots.NdbConfig(tolerance=0.0, max_iters=10))
+    yo, zo, ro = core.batched_newton_db(a, 0.0, 10)
+    for i in range(2):
+        err = np.linalg.norm(y[i] - yo[i]) / np.linalg.norm(yo[i])
+        print("ndb", b, i, err)
+        assert err < 5e-5, (b, i, err)
+print("ok")
+"""
+
+F16_SCRIPT = r"""
+import numpy as np
+from paper_2602_02016_b200 import roots
+from paper_2602_02016_b200.linalg import PrecisionMode
+from oracle import core
+for b in (384, 1024):
+    a = np.stack([core.random_spd(b, c, seed=i, scale=0.5) for i, c in enumerate([10.0, 1e2])])
+    y, z, rep = roots.batched_newton_db(a, roots.NdbConfig(tolerance=0.0, max_iters=10), PrecisionMode.F16)
+    yo, zo, ro = core.batched_newton_db(a, 0.0, 10)
+    for i in range(2):
+        ey = np.linalg.norm(y[i] - yo[i]) / np.linalg.norm(yo[i])
+        ez = np.linalg.norm(z[i] - zo[i]) / np.linalg.norm(zo[i])
+        print("ndb-f16", b, i, ey, ez)
+        assert ey < F16_BOUND and ez < F16_BOUND, (b, i, ey, ez)
 print("ok")
 """
 
 
-@pytest.mark.parametrize("env", [{"DASH_KB": "32"}, {"DASH_NACC": "1"}, {"DASH_NACC": "4"}])
-def test_engine_variant(env):
+def _run(script, env):
     import torch
 
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", SCRIPT], cwd=root, env={**os.environ, **env, "PYTHONPATH": root},
+    r = subprocess.run([sys.executable, "-c", script], cwd=root, env={**os.environ, **env, "PYTHONPATH": root},
                        capture_output=True, text=True, timeout=600)
+    print(r.stdout)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("env", [{"DASH_KB": "32"}, {"DASH_NACC": "1"}, {"DASH_NACC": "4"}, {"DASH_NT": "2562"}])
+def test_engine_variant(env):
+    _run(SCRIPT, env)
+
+
+@pytest.mark.parametrize("env", [{}, {"DASH_NT": "128"}])
+def test_f16_solver_tilings(env):
+    """fp16 products (one tensor pass, 11-bit operands): Newton-DB at B = 384 / 1024 within 1e-2 of float64."""
+    _run(F16_SCRIPT.replace("F16_BOUND", "1e-2"), env)
