@@ -11,6 +11,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -111,7 +112,7 @@ __device__ __forceinline__ void store_split(__half* hi, long long plane, int ld,
 // in the block) run only the tiles on or above the block diagonal; the epilogue stores each strictly-upper
 // 128 x 128 sub-block twice (direct and transposed) and drops the one below-diagonal sub-block of each
 // diagonal tile, so every output element has exactly one writer (deterministic).
-constexpr int kPairM = kTileM, kPairN = kTileN, kHalf = kTileM / 2, kHalfN = kTileN / 2;
+constexpr int kPairM = kTileM, kHalf = kTileM / 2;
 constexpr int kNaccDefault = 2;   // split-f16 accumulators per tile (env DASH_NACC = 1, 2 = main + correction, 4)
 constexpr int kEpiWarps = 8;     // 2 per TMEM lane quarter, 64 columns each
 constexpr int kSlots = 4;         // TMEM accumulator slots (4 x 128 columns = all 512)
@@ -126,16 +127,23 @@ constexpr int kThreads2 = 64 + 32 * kEpiWarps;
 // 256 x 128 tile needs ~156 B/clk of the 128 B/clk an SM's shared memory delivers for split products) at the
 // price of one accumulator per tile (2 TMEM sets of 256 columns), so it serves fp16 launches and split
 // launches that accept single-accumulator error.
+#ifndef DASH_P3_STAGES  // experiment overrides (build-time)
+#define DASH_P3_STAGES 3
+#endif
+#ifndef DASH_EPI_WARP_BYTES
+#define DASH_EPI_WARP_BYTES 8192
+#endif
 template <int PASSES, int KB, int NT = 128>
 struct Gemm2Cfg {
   static constexpr int kPlanes = PASSES == 3 ? 2 : 1;
   static constexpr int kABytes = kHalf * KB * 2;         // 16 / 8 KB per plane (128 rows of A)
   static constexpr int kBBytes = (NT / 2) * KB * 2;      // 8 / 4 KB per plane per 64 rows of B (NT / 2 rows)
   static constexpr int kStageBytes = (kABytes + kBBytes) * kPlanes;
-  static constexpr int kEpiBytes = kEpiWarps * 8192;  // per epilogue warp: 32 x 64 split tile (2 planes)
+  static constexpr int kEpiBytes = kEpiWarps * DASH_EPI_WARP_BYTES;  // per epilogue warp: 32 x 64 split tile (2 planes)
   // NT = 256: as many stages as the 227 KB of shared memory holds
-  static constexpr int kStages = NT == 128 ? (PASSES == 3 ? 3 : 6) * (64 / KB)
-                                           : (232448 - kEpiBytes - 1024 - 512) / kStageBytes;
+  static constexpr int kStages = NT == 128 ? (PASSES == 3 ? DASH_P3_STAGES : 6) * (64 / KB)
+                                           : ((232448 - kEpiBytes - 1024 - 512) / kStageBytes < 10
+                                                  ? (232448 - kEpiBytes - 1024 - 512) / kStageBytes : 10);
   static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 + 512;
   static_assert(kSmemBytes <= 232448, "shared memory per CTA");
   static_assert((2 * kStages + 2 * kSlots + kEpiWarps + 2 * kRing) * 8 + kRing * 4 + 4 <= 512, "barrier block");
@@ -442,14 +450,19 @@ template <int PASSES, int KB, int NT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     dash_gemm2_kernel(const GemmJob* __restrict__ jobs, int njobs, int total_tiles,
                       const CUtensorMap* __restrict__ maps, const int* __restrict__ gate, int nacc_in, int uniform,
-                      int* __restrict__ tile_counter) {
+                      int* __restrict__ tile_counter, unsigned long long* __restrict__ prof) {
+  // prof (DASH_GEMM_DEBUG & 2, diagnostics): clock64 cycles per role spent waiting on each barrier kind:
+  // [0] producer on empty, [1] MMA on tempty, [2] MMA on full, [3] epilogue on tfull, [4] epilogue on
+  // bulk-store reads, [5] producer total, [6] MMA total, [7] epilogue total (summed over warps)
+  unsigned long long pw0 = 0, pw1 = 0;
+  const long long t_start = clock64();
   using C = Gemm2Cfg<PASSES, KB, NT>;
   constexpr int kPN = NT;                    // pair tile columns = TMEM columns per accumulator slot
   constexpr int kRounds = NT / 128;          // epilogue passes over a tile (128 columns each)
   constexpr uint32_t kSl = 512 / NT;         // TMEM slots
   const int nacc = NT == 128 ? (nacc_in & 0xff) : 1;  // accumulators per tile (1, 2 or 4; 1 for NT = 256)
   const bool mc = PASSES == 3 && nacc == 2;  // main (hi*hi) + correction (hi*lo + lo*hi) accumulators
-  const int xp = nacc_in >> 8;  // DASH_EXP knobs: timing 1 hi planes only, 2 no epilogue, 4 no staging, 8 no bulk stores, 16 L2 prefetch; 32 mirror via global stores (valid, 2-3% slower)
+  const int xp = nacc_in >> 8;  // DASH_EXP knobs: timing 1 hi planes only, 2 no epilogue, 4 no staging, 8 no bulk stores, 16 L2 prefetch; 32 mirror via global stores (valid, 2-3% slower); 64 / 128 plain (unhinted) split stores / operand loads
   const uint32_t nsets = kSl / nacc;         // tiles in flight in TMEM
 
   if (gate && *gate == 0) return;  // uniform across the grid (and thus across each pair)
@@ -509,6 +522,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       uint32_t phase = 0;
       const uint32_t peer_ring = mapa_shared(smem_u32(tile_ring), 1);
       const uint32_t peer_full = mapa_shared(smem_u32(tq_full), 1);
+      const uint64_t pol_load = l2_policy_evict_last();
       for (uint32_t it = 0;; ++it) {
         int tile;
         if (rank == 0) {
@@ -562,29 +576,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
           for (int kb = 0; kb < kPrefetch && kb < nk; ++kb) prefetch(kb);
         for (int kb = 0; kb < nk; ++kb) {
           if ((xp & 16) && kb + kPrefetch < nk) prefetch(kb + kPrefetch);
-          mbar_wait(&empty[stage], phase ^ 1);
+          {
+            const long long w0 = prof ? clock64() : 0;
+            mbar_wait(&empty[stage], phase ^ 1);
+            if (prof) pw0 += clock64() - w0;
+          }
           const int nplanes = (xp & 1) ? 1 : C::kPlanes;  // experiment knob: hi planes only (timing)
           if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * C::kStageBytes / C::kPlanes * nplanes);
           uint8_t* sA = smem + stage * C::kStageBytes;
           uint8_t* sB = sA + C::kABytes * C::kPlanes;
           const int k0 = kb * KB;
+          auto load = [&](void* dst, const CUtensorMap* map, int x0, int x1, int pl, int mat) {
+            if (!(xp & 128)) tma2_load_4d_hint(dst, map, &full[stage], x0, x1, pl, mat, pol_load);  // L2 evict-last
+            else tma2_load_4d(dst, map, &full[stage], x0, x1, pl, mat);
+          };
 #pragma unroll
           for (int p = 0; p < C::kPlanes; ++p) {
             if (p >= nplanes) break;
             uint8_t* a_dst = sA + p * C::kABytes;
             uint8_t* b_dst = sB + p * C::kBBytes;
             if (!a_mn) {
-              tma2_load_4d(a_dst, amap, &full[stage], k0, am, p, a_mat);
+              load(a_dst, amap, k0, am, p, a_mat);
             } else {
-              tma2_load_4d(a_dst, amap, &full[stage], am, k0, p, a_mat);
-              tma2_load_4d(a_dst + 64 * KB * 2, amap, &full[stage], am + 64, k0, p, a_mat);
+              load(a_dst, amap, am, k0, p, a_mat);
+              load(a_dst + 64 * KB * 2, amap, am + 64, k0, p, a_mat);
             }
             // B: NT / 2 rows per CTA as 64-row boxes (K-major: consecutive 8-row groups; MN-major: 64-column
             // groups KB * 128 B apart, the LBO of the descriptor)
 #pragma unroll
             for (int h = 0; h < NT / 128; ++h) {
-              if (!b_mn) tma2_load_4d(b_dst + h * 64 * KB * 2, bmap, &full[stage], k0, bn + 64 * h, p, b_mat);
-              else tma2_load_4d(b_dst + h * 64 * KB * 2, bmap, &full[stage], bn + 64 * h, k0, p, b_mat);
+              if (!b_mn) load(b_dst + h * 64 * KB * 2, bmap, k0, bn + 64 * h, p, b_mat);
+              else load(b_dst + h * 64 * KB * 2, bmap, bn + 64 * h, k0, p, b_mat);
             }
           }
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
@@ -623,12 +645,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
           const bool first = kin == 0;
           const uint32_t slot = base + static_cast<uint32_t>(c);
           if (first) {
+            const long long w0 = prof ? clock64() : 0;
             mbar_wait(&tempty[slot], use_par);
             if (mc) mbar_wait(&tempty[slot + 1], use_par);
+            if (prof) pw0 += clock64() - w0;
             tc_fence_after();
           }
           const uint32_t d_tmem = tmem_base + slot * kPN;
-          mbar_wait(&full[stage], phase);
+          {
+            const long long w0 = prof ? clock64() : 0;
+            mbar_wait(&full[stage], phase);
+            if (prof) pw1 += clock64() - w0;
+          }
           tc_fence_after();
           const uint32_t a_base = smem_u32(smem + stage * C::kStageBytes);
           const uint32_t b_base = a_base + C::kABytes * C::kPlanes;
@@ -672,6 +700,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     uint8_t* ebuf = smem + C::kStages * C::kStageBytes + (warp - 2) * 8192;  // 1024-aligned staging tile
     uint32_t sphase = 0;
     const uint32_t leader_tempty = mapa_shared(smem_u32(tempty), 0);
+    const uint64_t pol_store = l2_policy_evict_first();
+    auto wait_reads = [&]() {  // lane 0: this warp's bulk stores have read the staging buffer
+      const long long w0 = prof ? clock64() : 0;
+      bulk_wait_read0();
+      if (prof) pw1 += clock64() - w0;
+    };
+    // split tile bulk store, L2 evict-first (its next reader is a later launch; keep the operands resident)
+    auto store4 = [&](int map, int x0, int x1, int mat) {
+      if (!(xp & 64)) tma_store_4d_hint(maps + map, ebuf, x0, x1, 0, mat, pol_store);
+      else tma_store_4d(maps + map, ebuf, x0, x1, 0, mat);
+    };
     uint32_t t = 0;
     for (;; ++t) {
       int tile = 0;
@@ -696,7 +735,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         const bool fin_tma = f_tma && jb.op == EPI_EMA;
         __syncwarp();                 // every lane is done with the previous tile's staging buffer
         if ((side_tma || fin_tma) && lane == 0) {  // stage the side / fp32 input tile while the MMAs run
-          bulk_wait_read0();          // the previous tile's bulk stores have read the buffer
+          wait_reads();          // the previous tile's bulk stores have read the buffer
           mbar_arrive_expect_tx(&sbar[warp - 2], 8192);
           const int tc0 = n0 + 64 * hc, tr0 = m0 + kHalf * static_cast<int>(rank) + 32 * q;
           if (side_tma) {
@@ -710,7 +749,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         for (int c = 0; c < nacc; ++c) {
           const uint32_t slot = base + static_cast<uint32_t>(c);
           if (rd == 0) {
+            const long long w0 = prof ? clock64() : 0;
             mbar_wait(&tfull[slot], use_par);
+            if (prof) pw0 += clock64() - w0;
             tc_fence_after();
           }
           if (c < used) {
@@ -797,25 +838,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
           const int lr = static_cast<int>(lane);
           auto ident = [](float v, int) { return v; };
           if (tma_out) {
-          if (lane == 0) bulk_wait_read0();  // this warp's previous stores have read the buffer
+          if (lane == 0) wait_reads();  // this warp's previous stores have read the buffer
           __syncwarp();                      // (and every lane is done with the staged side input)
           if (!(xp & 4)) stage_direct(ebuf, acc, lr, c0, cx.inv_out, ident, cx.ovf);
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0 && !(xp & 8)) {
-            tma_store_4d(maps + jb.c_map, ebuf, c0, r0, 0, jb.c_mat);
+            store4(jb.c_map, c0, r0, jb.c_mat);
             bulk_commit();
           }
           if (cx.mirror && (xp & 32)) {
             store_mirror_from_stage(ebuf, jb.c_hi, jb.c_plane, jb.c_ld, r0, c0, cx.N, lr);
           } else if (cx.mirror) {
-            if (lane == 0) bulk_wait_read0();
+            if (lane == 0) wait_reads();
             __syncwarp();
             stage_transpose_in_place(ebuf, lr);
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_4d(maps + jb.c_tmap, ebuf, r0, c0, 0, jb.c_mat);
+              store4(jb.c_tmap, r0, c0, jb.c_mat);
               bulk_commit();
             }
           }
@@ -827,32 +868,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
               const float d = (r == col) ? 1.f : 0.f;
               return inact ? d : ca * d - cb * m;
             };
-            if (lane == 0) bulk_wait_read0();
+            if (lane == 0) wait_reads();
             __syncwarp();
             stage_direct(ebuf, acc, lr, c0, cx.inv_e, corr, cx.ovf2);
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_4d(maps + jb.c2_map, ebuf, c0, r0, 0, jb.c2_mat);
+              store4(jb.c2_map, c0, r0, jb.c2_mat);
               bulk_commit();
             }
             if (cx.mirror && (xp & 32)) {
               store_mirror_from_stage(ebuf, jb.c2_hi, jb.c2_plane, jb.c_ld, r0, c0, cx.N, lr);
             } else if (cx.mirror) {
-              if (lane == 0) bulk_wait_read0();
+              if (lane == 0) wait_reads();
               __syncwarp();
               stage_transpose_in_place(ebuf, lr);
               fence_proxy_async_smem();
               __syncwarp();
               if (lane == 0) {
-                tma_store_4d(maps + jb.c2_tmap, ebuf, r0, c0, 0, jb.c2_mat);
+                store4(jb.c2_tmap, r0, c0, jb.c2_mat);
                 bulk_commit();
               }
             }
           }
           }  // tma_out
           if (f_tma) {  // fp32 output: direct tile (two swizzled 32 x 32 boxes) and, if symmetric, its mirror
-            if (lane == 0) bulk_wait_read0();
+            if (lane == 0) wait_reads();
             __syncwarp();
             stage_direct_f32(ebuf, acc, lr);
             fence_proxy_async_smem();
@@ -863,7 +904,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
               bulk_commit();
             }
             if (cx.mirror) {
-              if (lane == 0) bulk_wait_read0();
+              if (lane == 0) wait_reads();
               __syncwarp();
               stage_transposed_f32(ebuf, acc, lr);
               fence_proxy_async_smem();
@@ -897,6 +938,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     }
     if (lane == 0) bulk_wait0();  // bulk stores complete before the CTA retires
   }
+  if (prof && lane == 0 && (warp >= 2 || warp == 0 || rank == 0)) {
+    const unsigned long long tot = clock64() - t_start;
+    if (warp == 0) { atomicAdd(prof + 0, pw0); atomicAdd(prof + 5, tot); }
+    else if (warp == 1) { atomicAdd(prof + 1, pw0); atomicAdd(prof + 2, pw1); atomicAdd(prof + 6, tot); }
+    else { atomicAdd(prof + 3, pw0); atomicAdd(prof + 4, pw1); atomicAdd(prof + 7, tot); }
+  }
   tc_fence_before();
   cluster_sync_all();  // no CTA of the pair may exit while its peer still uses its TMEM / barriers
   if (warp == 1) {
@@ -929,7 +976,8 @@ void note_launch(int n) { g_launches += static_cast<unsigned long long>(n); }
 
 template <int PASSES, int KB, int NT = 128>
 static void launch_variant(int grid2, cudaStream_t stream, const GemmJob* d_jobs, int njobs, int total_tiles,
-                           const CUtensorMap* d_maps, const int* gate, int flags, int uniform, int* counter) {
+                           const CUtensorMap* d_maps, const int* gate, int flags, int uniform, int* counter,
+                           unsigned long long* prof) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(dash_gemm2_kernel<PASSES, KB, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -937,7 +985,7 @@ static void launch_variant(int grid2, cudaStream_t stream, const GemmJob* d_jobs
     attr = true;
   }
   dash_gemm2_kernel<PASSES, KB, NT><<<grid2, kThreads2, Gemm2Cfg<PASSES, KB, NT>::kSmemBytes, stream>>>(
-      d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter);
+      d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter, prof);
 }
 
 // Per-stream pair of device counters (tile counter, finished pairs) for the dynamic tile scheduler; the
@@ -1014,6 +1062,11 @@ int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtenso
   cudaError_t err;
   const int grid2 = 2 * (total_tiles < g_num_sms / 2 ? total_tiles : g_num_sms / 2);  // CTA pairs
   int* counter = tile_counter_for(stream);
+  static unsigned long long* prof = nullptr;
+  if ((g_dbg & 2) && !prof) {
+    cudaMalloc(&prof, 8 * sizeof(unsigned long long));
+    cudaMemset(prof, 0, 8 * sizeof(unsigned long long));
+  }
   if (!counter) return 3;
   (void)grid;
   if (g_kb == 0) {
@@ -1022,15 +1075,27 @@ int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtenso
     if (g_kb != 32 && g_kb != 64) g_kb = kKbDefault;
   }
   const int flags = (passes == 3 ? g_nacc : 1) | (g_exp << 8);
-  if (use_wide && passes == 3 && g_kb == 64) launch_variant<3, 64, 256>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter);
-  else if (use_wide && passes == 3) launch_variant<3, 32, 256>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter);
-  else if (use_wide && g_kb == 64) launch_variant<1, 64, 256>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter);
-  else if (use_wide) launch_variant<1, 32, 256>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter);
-  else if (passes == 3 && g_kb == 64) launch_variant<3, 64>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter);
-  else if (passes == 3) launch_variant<3, 32>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter);
-  else if (g_kb == 64) launch_variant<1, 64>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter);
-  else launch_variant<1, 32>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter);
+  if (use_wide && passes == 3 && g_kb == 64) launch_variant<3, 64, 256>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter, prof);
+  else if (use_wide && passes == 3) launch_variant<3, 32, 256>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter, prof);
+  else if (use_wide && g_kb == 64) launch_variant<1, 64, 256>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter, prof);
+  else if (use_wide) launch_variant<1, 32, 256>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter, prof);
+  else if (passes == 3 && g_kb == 64) launch_variant<3, 64>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter, prof);
+  else if (passes == 3) launch_variant<3, 32>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter, prof);
+  else if (g_kb == 64) launch_variant<1, 64>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter, prof);
+  else launch_variant<1, 32>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter, prof);
   if (e1) cudaEventRecord(e1, stream);
+  if (prof) {  // diagnostics: per-launch wait-cycle breakdown (serialises the stream)
+    unsigned long long h[8];
+    cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, stream);
+    cudaStreamSynchronize(stream);
+    cudaMemsetAsync(prof, 0, sizeof(h), stream);
+    auto pct = [](unsigned long long a, unsigned long long b) { return b ? 100.0 * a / b : 0.0; };
+    fprintf(stderr,
+            "[gemm] passes=%d nt=%d tiles=%d  producer: empty-wait %.1f%%  mma: tempty-wait %.1f%% full-wait %.1f%%"
+            "  epilogue: tfull-wait %.1f%% store-read-wait %.1f%%\n",
+            passes, use_wide ? 256 : 128, total_tiles, pct(h[0], h[5]), pct(h[1], h[6]), pct(h[2], h[6]),
+            pct(h[3], h[7]), pct(h[4], h[7]));
+  }
   err = cudaGetLastError();
   return err == cudaSuccess ? 0 : 3;
 }
