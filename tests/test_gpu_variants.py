@@ -35,6 +35,27 @@ for b in (200, 384):  # 384: two row tiles, a ragged last column tile in both ti
 print("ok")
 """
 
+F16_CN_CHEB_SCRIPT = r"""
+import numpy as np
+from paper_2602_02016_b200 import chebyshev, roots
+from paper_2602_02016_b200.linalg import PrecisionMode
+from oracle import core
+c = chebyshev.fit_inverse_root(4)
+for b in (384, 1024):  # CN: two split outputs (M, correction) per job; Clenshaw: TMA-staged side input B_{k+2}
+    a = np.stack([core.random_spd(b, cnd, seed=20 + i, scale=0.5) for i, cnd in enumerate([10.0, 1e2])])
+    x, rep = roots.batched_coupled_newton(a, roots.CnConfig(p=4, tolerance=0.0, max_iters=12), PrecisionMode.F16)
+    xo, ro = core.batched_coupled_newton(a, 4, 0.0, 12)
+    sc = 2.0 * np.linalg.eigvalsh(a)[:, -1]
+    y = chebyshev.batched_clenshaw_matrix(a, c, sc, PrecisionMode.F16)
+    yo = core.batched_clenshaw(a, c.coeffs, sc, 4)
+    for i in range(2):
+        ex = np.linalg.norm(x[i] - xo[i]) / np.linalg.norm(xo[i])
+        ey = np.linalg.norm(y[i] - yo[i]) / np.linalg.norm(yo[i])
+        print("cn/cheb-f16", b, i, ex, ey)
+        assert ex < 1e-2 and ey < 2e-2, (b, i, ex, ey)
+print("ok")
+"""
+
 F16_SCRIPT = r"""
 import numpy as np
 from paper_2602_02016_b200 import roots
@@ -68,6 +89,12 @@ def _run(script, env):
 @pytest.mark.parametrize("env", [{"DASH_KB": "32"}, {"DASH_NACC": "1"}, {"DASH_NACC": "4"}, {"DASH_NT": "2562"}])
 def test_engine_variant(env):
     _run(SCRIPT, env)
+
+
+@pytest.mark.parametrize("env", [{}, {"DASH_NT": "128"}])
+def test_f16_cn_chebyshev_tilings(env):
+    """Coupled Newton (p = 4) and Clenshaw in fp16 mode under both tilings vs float64."""
+    _run(F16_CN_CHEB_SCRIPT, env)
 
 
 @pytest.mark.parametrize("env", [{}, {"DASH_NT": "128"}])
