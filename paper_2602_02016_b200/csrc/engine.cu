@@ -180,6 +180,7 @@ bool JobBuilder::operands(GemmJob& j, const dash_stack& a, int am, int trans_a, 
   j.b_mn = trans_b ? 0 : 1;  // stored K x N -> MN-major; stored N x K -> K-major
   j.a_map = add_map(a, j.a_mn ? 64 : kTileM / 2);  // each CTA of the pair: 128 rows of A, 64 rows of B
   j.b_map = add_map(b, 64);
+  j.a_mapT = add_map(a, j.a_mn ? kTileM / 2 : 64);  // the other majorness (upper pair-block storage reads)
   // K-block 32 variant (deeper pipeline): K-major boxes 32 wide with 64-byte swizzle, MN-major boxes 32 deep
   j.a_map32 = j.a_mn ? add_map(a, 32, 64, 1, 128) : add_map(a, kTileM / 2, 32, 1, 64);
   j.b_map32 = j.b_mn ? add_map(b, 32, 64, 1, 128) : add_map(b, 64, 32, 1, 64);

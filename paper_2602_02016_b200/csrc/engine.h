@@ -27,6 +27,7 @@ int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtenso
                 cudaStream_t stream, const int* gate = nullptr, double flops = 0.0, int uniform = 0,
                 double issued = 0.0, const GemmWide* wide = nullptr);
 void note_launch(int n = 1);  // count non-GEMM kernel launches
+int gemm_kblock();            // K-block of the GEMM launches (64, or 32 under DASH_KB=32)
 extern unsigned long long g_launches;
 void gemm_timing_enable(int on);
 int gemm_timing_read(int* n, double* ms, double* flops);

@@ -149,6 +149,10 @@ struct Gemm2Cfg {
   static_assert((2 * kStages + 2 * kSlots + kEpiWarps + 2 * kRing) * 8 + kRing * 4 + 4 <= 512, "barrier block");
 };
 
+// Upper pair-block storage: is the k-block (256-block kp) of an operand whose 256-row/col block is `blk` a
+// lower block?  K-major operands are stored (rows = blk, cols = k); MN-major ones (rows = k, cols = blk).
+__device__ __forceinline__ bool upper_flip(int mn, int blk, int kp) { return mn ? kp > blk : blk > kp; }
+
 // Tile `local` of a job -> (256-row tile ti, NT-column tile tj).  Symmetric jobs enumerate, per row tile
 // I, only the column tiles that reach the diagonal: J >= 2I (NT = 128) or J >= I (NT = 256).
 template <int NT>
@@ -554,7 +558,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         const int nk = (jb.K + KB - 1) / KB;
         const CUtensorMap* amap = maps + (KB == 64 ? jb.a_map : jb.a_map32);
         const CUtensorMap* bmap = maps + (KB == 64 ? jb.b_map : jb.b_map32);
+        const CUtensorMap* amapT = maps + jb.a_mapT;
         const int a_mn = jb.a_mn, b_mn = jb.b_mn, a_mat = jb.a_mat, b_mat = jb.b_mat;
+        const int a_up = KB == 64 ? jb.a_up : 0, b_up = KB == 64 ? jb.b_up : 0;
         // L2 prefetch kPrefetch k-blocks beyond the shared-memory ring: the ring only covers ~3 k-blocks of
         // MMA time, less than an HBM miss, and every tile's first touch of an operand block misses L2
         auto prefetch = [&](int kb) {
@@ -590,22 +596,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             if (!(xp & 128)) tma2_load_4d_hint(dst, map, &full[stage], x0, x1, pl, mat, pol_load);  // L2 evict-last
             else tma2_load_4d(dst, map, &full[stage], x0, x1, pl, mat);
           };
+          // upper pair-block storage: a lower k-block is read as the transposed upper one (other majorness)
+          const bool fa = a_up && upper_flip(a_mn, ti, k0 >> 8);
+          const bool fb = b_up && upper_flip(b_mn, bn >> 8, k0 >> 8);
+          const int ea_mn = a_mn ^ static_cast<int>(fa), eb_mn = b_mn ^ static_cast<int>(fb);
+          const CUtensorMap* am_cur = fa ? amapT : amap;
 #pragma unroll
           for (int p = 0; p < C::kPlanes; ++p) {
             if (p >= nplanes) break;
             uint8_t* a_dst = sA + p * C::kABytes;
             uint8_t* b_dst = sB + p * C::kBBytes;
-            if (!a_mn) {
-              load(a_dst, amap, k0, am, p, a_mat);
+            if (!ea_mn) {
+              load(a_dst, am_cur, k0, am, p, a_mat);
             } else {
-              load(a_dst, amap, am, k0, p, a_mat);
-              load(a_dst + 64 * KB * 2, amap, am + 64, k0, p, a_mat);
+              load(a_dst, am_cur, am, k0, p, a_mat);
+              load(a_dst + 64 * KB * 2, am_cur, am + 64, k0, p, a_mat);
             }
             // B: NT / 2 rows per CTA as 64-row boxes (K-major: consecutive 8-row groups; MN-major: 64-column
             // groups KB * 128 B apart, the LBO of the descriptor)
 #pragma unroll
             for (int h = 0; h < NT / 128; ++h) {
-              if (!b_mn) load(b_dst + h * 64 * KB * 2, bmap, k0, bn + 64 * h, p, b_mat);
+              if (!eb_mn) load(b_dst + h * 64 * KB * 2, bmap, k0, bn + 64 * h, p, b_mat);
               else load(b_dst + h * 64 * KB * 2, bmap, bn + 64 * h, k0, p, b_mat);
             }
           }
@@ -627,17 +638,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         if (tile < 0) break;
         const GemmJob& jb = jobs[find_job<NT>(jobs, njobs, tile, uniform)];
         const int nk = (jb.K + KB - 1) / KB;
+        int ti, tj;
+        tile_coords<NT>(jb, tile - job_tile_start<NT>(jb), ti, tj);
+        const int a_up = KB == 64 ? jb.a_up : 0, b_up = KB == 64 ? jb.b_up : 0;
+        const int bpb = (tj * kPN) >> 8;  // 256-block of this tile's B rows (the same for both CTAs)
         // main + correction mode (nacc == 2, split products): hi*hi -> slot 0, hi*lo + lo*hi -> slot 1 over the
         // whole K; otherwise slot c takes the k-blocks [c*per, (c+1)*per)
         const int per = mc ? nk : (nk + nacc - 1) / nacc;
-        const uint32_t idesc = umma_idesc_f16(kPairM, kPN, jb.a_mn, jb.b_mn);
         // K-major: 128-byte (KB 64) or 64-byte (KB 32) swizzled rows, 8-row groups 1024 / 512 B apart, 32 B per
         // 16-wide k step; MN-major: 128-byte rows along M/N, 64-column groups KB * 128 B apart, 2 KB per k step
         constexpr uint32_t kSbo = KB == 64 ? 1024u : 512u, kLay = KB == 64 ? 2u : 4u;
-        const uint32_t a_lbo = jb.a_mn ? KB * 128u : 16u, b_lbo = jb.b_mn ? KB * 128u : 16u;
-        const uint32_t a_kstep = jb.a_mn ? 2048u : 32u, b_kstep = jb.b_mn ? 2048u : 32u;
-        const uint32_t a_sbo = jb.a_mn ? 1024u : kSbo, b_sbo = jb.b_mn ? 1024u : kSbo;
-        const uint32_t a_lay = jb.a_mn ? 2u : kLay, b_lay = jb.b_mn ? 2u : kLay;
         const uint32_t base = (t % nsets) * static_cast<uint32_t>(nacc);
         const uint32_t use_par = ((t / nsets) & 1u) ^ 1u;
         int c = 0, kin = 0;  // accumulator slot, k-block index within the slot's K range
@@ -652,6 +662,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             tc_fence_after();
           }
           const uint32_t d_tmem = tmem_base + slot * kPN;
+          // operand majorness of this k-block (flipped for lower blocks of upper pair-block storage)
+          const int a_mn = jb.a_mn ^ static_cast<int>(a_up && upper_flip(jb.a_mn, ti, (kb * KB) >> 8));
+          const int b_mn = jb.b_mn ^ static_cast<int>(b_up && upper_flip(jb.b_mn, bpb, (kb * KB) >> 8));
+          const uint32_t idesc = umma_idesc_f16(kPairM, kPN, a_mn, b_mn);
+          const uint32_t a_lbo = a_mn ? KB * 128u : 16u, b_lbo = b_mn ? KB * 128u : 16u;
+          const uint32_t a_kstep = a_mn ? 2048u : 32u, b_kstep = b_mn ? 2048u : 32u;
+          const uint32_t a_sbo = a_mn ? 1024u : kSbo, b_sbo = b_mn ? 1024u : kSbo;
+          const uint32_t a_lay = a_mn ? 2u : kLay, b_lay = b_mn ? 2u : kLay;
           {
             const long long w0 = prof ? clock64() : 0;
             mbar_wait(&full[stage], phase);
@@ -781,7 +799,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         // symmetric job: this CTA's 128 x 128 sub-block (row block 2 ti + rank, column block n0 / 128)
         const int rb = 2 * ti + static_cast<int>(rank), cb = n0 / 128;
         cx.store = !jb.sym || rb <= cb;
-        cx.mirror = jb.sym && rb < cb;
+        cx.mirror = jb.sym && rb < cb && (!jb.c_up || (rb >> 1) == (cb >> 1));
         cx.row_ok = cx.r < jb.M && cx.store;
         const int ea = jb.a_exp ? __ldg(jb.a_exp) : 0;
         const int eb = jb.b_exp ? __ldg(jb.b_exp) : 0;
@@ -999,6 +1017,15 @@ static int* tile_counter_for(cudaStream_t stream) {
   if (cudaMemset(p, 0, 2 * sizeof(int)) != cudaSuccess) return nullptr;
   table.emplace_back(stream, p);
   return p;
+}
+
+int gemm_kblock() {
+  if (g_kb == 0) {
+    const char* e = getenv("DASH_KB");
+    g_kb = e ? atoi(e) : kKbDefault;
+    if (g_kb != 32 && g_kb != 64) g_kb = kKbDefault;
+  }
+  return g_kb;
 }
 
 // 256-wide pair tiles (DASH_NT): 0 never, 1 fp16 launches (default), 2 fp16 and split launches

@@ -343,6 +343,39 @@ static void copy_stack_if(const int* par, int want, const dash_stack& dst, const
 // cond-1e3 block then trips the divergence watch in tolerance mode (iteration 17, residual 6e-3).
 static const int kSymB = getenv("DASH_SYMB") ? atoi(getenv("DASH_SYMB")) : 0;
 
+// Upper pair-block storage of the Newton iterates (types.h): the iterates Y, Z, E are symmetric, so the
+// launches store only the 256x256 pair blocks on/above the diagonal and read lower operand blocks transposed
+// (K-block 64 launches only; DASH_NDB_UP=0 stores full matrices).  The solver's outputs are completed at the
+// end by fill_lower_kernel.
+static bool ndb_upper_storage() {
+  static const int on = getenv("DASH_NDB_UP") ? atoi(getenv("DASH_NDB_UP")) : 1;
+  return on && gemm_kblock() == 64;
+}
+
+// Lower pair blocks of an upper-stored split stack <- transposes of the upper ones (both planes), through
+// 32x32 shared-memory tiles (coalesced reads and writes).
+__global__ void fill_lower_kernel(dash_stack s) {
+  __shared__ uint16_t t[32][33];
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;  // destination tile (lower pair block)
+  if ((r0 >> 8) <= (c0 >> 8)) return;
+  uint16_t* base = reinterpret_cast<uint16_t*>(s.data) + static_cast<size_t>(blockIdx.z) * s.rows * s.ld;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int r = c0 + i, c = r0 + static_cast<int>(threadIdx.x);
+    t[i][threadIdx.x] = (r < s.rows && c < s.cols) ? base[static_cast<size_t>(r) * s.ld + c] : 0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int r = r0 + i, c = c0 + static_cast<int>(threadIdx.x);
+    if (r < s.rows && c < s.cols) base[static_cast<size_t>(r) * s.ld + c] = t[threadIdx.x][i];
+  }
+}
+
+static void fill_lower(const dash_stack& s, cudaStream_t st) {
+  const dim3 grid((s.cols + 31) / 32, (s.rows + 31) / 32, 2 * s.nmat);
+  fill_lower_kernel<<<grid, dim3(32, 8), 0, st>>>(s);
+  note_launch();
+}
+
 // ---------------------------------------------------------------------------- NDB
 size_t ndb_ws_bytes(int n, int b) {  // NOLINT
   const size_t stacks = 3 * stack_bytes(n, b, b);
@@ -364,6 +397,7 @@ int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_o
   const dash_stack ys[2] = {y_out, y2};
   const dash_stack zs[2] = {z_out, z2};
   UploadedGemm g_first, g_e[2], g_yz[2];
+  const int up = ndb_upper_storage() ? 1 : 0;
   {
     JobBuilder jb;  // Y1 = (a E1) * inv_scale
     for (int m = 0; m < n; ++m) {
@@ -372,6 +406,7 @@ int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_o
       j.op = EPI_SPLIT;
       j.out_mat = m;
       j.sym = 1;
+      j.c_up = up;
       j.alpha_p = inv_scale;
       jb.set_out(j, ys[1], m);
       jb.push(j);
@@ -390,6 +425,7 @@ int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_o
       j.op = EPI_NDB_E;
       j.out_mat = m;
       j.sym = 1;
+      j.a_up = j.b_up = j.c_up = up;
       j.active = s.active;
       j.resid = s.resid;
       je.set_out(j, e, m);
@@ -403,12 +439,14 @@ int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_o
       j.op = EPI_SPLIT;
       j.out_mat = m;
       j.sym = 1;
+      j.a_up = j.b_up = j.c_up = up;
       jy.set_out(j, yn, m);
       jy.push(j);
       if (!jy.operands(j, e, m, 0, zc, m, kSymB)) return DASH_EINVAL;
       j.op = EPI_SPLIT;
       j.out_mat = m;
       j.sym = 1;
+      j.a_up = j.b_up = j.c_up = up;
       jy.set_out(j, zn, m);
       jy.push(j);
     }
@@ -444,6 +482,10 @@ int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_o
   note_launch();
   copy_stack_if(s.par, 1, y_out, y2, st);  // final iterate in the scratch pair -> outputs
   copy_stack_if(s.par, 1, z_out, z2, st);
+  if (up) {
+    fill_lower(y_out, st);
+    fill_lower(z_out, st);
+  }
   if (products) *products = np;
   return cuda_ok();
 }

@@ -56,6 +56,12 @@ struct GemmJob {
   int f_ld;        // fp32 output / input leading dim
   int s_ld;        // side split input leading dim
   int sym;         // 1: C is symmetric (M == N): only tiles on/above the diagonal run, the epilogue mirrors
+  // Upper pair-block storage of symmetric matrices (K-block 64 launches): a stack flagged `up` holds only the
+  // 256x256 pair blocks on or above the block diagonal (diagonal pair blocks complete).  a_up / b_up: read a
+  // lower k-block of the operand as the transposed upper one (a_mapT = the A map of the other majorness;
+  // B uses the same 64x64 map with swapped coordinates).  c_up: the epilogue mirrors only inside diagonal
+  // pair blocks.
+  int a_up, b_up, c_up, a_mapT;
   const int* a_exp;  const unsigned* a_amax;   // exponent / amax of the A matrix
   const int* b_exp;  const unsigned* b_amax;
   // ---- TMA store maps of the split outputs (-1: direct stores): c_map / c2_map box 64 x 32 x 2 planes
