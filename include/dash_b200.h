@@ -90,6 +90,14 @@ int dash_ndb(const dash_stack* a, const float* inv_scale, const dash_stack* y, c
              void* stream);
 /* dash_cn: batched coupled Newton (roots.batched_coupled_newton, roots.py:216-259): x <- a_hat^(-1/p),
  *   p in {2, 4}, c = CnConfig.resolved_c (roots.py:53-56). */
+/* dash_ndb_upper: dash_ndb leaving y and z in upper pair-block storage (only the 256x256 blocks on or above
+ *   the block diagonal are valid, diagonal blocks complete) -- the optimizer completes only the
+ *   output it reads.  dash_fill_lower completes such a stack in place (lower blocks <- transposed upper);
+ *   both are plain dash_ndb / a no-op when the iterates are stored complete (DASH_NDB_UP=0, DASH_KB=32). */
+int dash_ndb_upper(const dash_stack* a, const float* inv_scale, const dash_stack* y, const dash_stack* z, float tol,
+                   int max_iters, int passes, int* iters, float* resid, int* conv, void* ws, size_t ws_bytes,
+                   void* stream);
+int dash_fill_lower(const dash_stack* s, void* stream);
 size_t dash_cn_ws_bytes(int n, int b);
 int dash_cn(const dash_stack* a, const float* inv_scale, int p, float c, const dash_stack* x, float tol,
             int max_iters, int passes, int* iters, float* resid, int* conv, void* ws, size_t ws_bytes,

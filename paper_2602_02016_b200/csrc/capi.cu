@@ -24,6 +24,22 @@ int dash_ndb(const dash_stack* a, const float* inv_scale, const dash_stack* y, c
                    static_cast<cudaStream_t>(stream), nullptr);
 }
 
+int dash_ndb_upper(const dash_stack* a, const float* inv_scale, const dash_stack* y, const dash_stack* z, float tol,
+                   int max_iters, int passes, int* iters, float* resid, int* conv, void* ws, size_t ws_bytes,
+                   void* stream) {
+  if (!square_same(a, y) || !square_same(a, z) || max_iters < 1 || tol < 0.f || !iters || !resid || !conv ||
+      (passes != 1 && passes != 3))
+    return DASH_EINVAL;
+  if (ws_bytes < ndb_ws_bytes(a->nmat, a->rows)) return DASH_EINVAL;
+  return ndb_solve(*a, inv_scale, *y, *z, tol, max_iters, passes, iters, resid, conv, ws, ws_bytes,
+                   static_cast<cudaStream_t>(stream), nullptr, false);
+}
+
+int dash_fill_lower(const dash_stack* s, void* stream) {
+  if (!stack_ok(s) || s->rows != s->cols) return DASH_EINVAL;
+  return fill_lower(*s, static_cast<cudaStream_t>(stream));
+}
+
 size_t dash_cn_ws_bytes(int n, int b) { return cn_ws_bytes(n, b); }
 
 int dash_cn(const dash_stack* a, const float* inv_scale, int p, float c, const dash_stack* x, float tol,

@@ -347,7 +347,7 @@ static const int kSymB = getenv("DASH_SYMB") ? atoi(getenv("DASH_SYMB")) : 0;
 // launches store only the 256x256 pair blocks on/above the diagonal and read lower operand blocks transposed
 // (K-block 64 launches only; DASH_NDB_UP=0 stores full matrices).  The solver's outputs are completed at the
 // end by fill_lower_kernel.
-static bool ndb_upper_storage() {
+bool ndb_upper_storage() {
   static const int on = getenv("DASH_NDB_UP") ? atoi(getenv("DASH_NDB_UP")) : 1;
   return on && gemm_kblock() == 64;
 }
@@ -370,10 +370,12 @@ __global__ void fill_lower_kernel(dash_stack s) {
   }
 }
 
-static void fill_lower(const dash_stack& s, cudaStream_t st) {
+int fill_lower(const dash_stack& s, cudaStream_t st) {
+  if (!ndb_upper_storage()) return DASH_OK;  // the iterates were stored complete
   const dim3 grid((s.cols + 31) / 32, (s.rows + 31) / 32, 2 * s.nmat);
   fill_lower_kernel<<<grid, dim3(32, 8), 0, st>>>(s);
   note_launch();
+  return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ECUDA;
 }
 
 // ---------------------------------------------------------------------------- NDB
@@ -385,7 +387,7 @@ size_t ndb_ws_bytes(int n, int b) {  // NOLINT
 
 int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_out, const dash_stack& z_out,
               float tol, int max_iters, int passes, int* iters, float* resid_out, int* conv, void* ws,
-              size_t ws_bytes, cudaStream_t st, int* products) {
+              size_t ws_bytes, cudaStream_t st, int* products, bool complete) {
   const int n = a.nmat;
   Arena ar(ws, ws_bytes);
   dash_stack e, y2, z2;
@@ -482,7 +484,7 @@ int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_o
   note_launch();
   copy_stack_if(s.par, 1, y_out, y2, st);  // final iterate in the scratch pair -> outputs
   copy_stack_if(s.par, 1, z_out, z2, st);
-  if (up) {
+  if (up && complete) {  // (complete = false: the caller completes only the outputs it reads)
     fill_lower(y_out, st);
     fill_lower(z_out, st);
   }

@@ -86,19 +86,29 @@ class DeviceReports:
 
 
 def ndb_split(a: SplitStack, inv_scale: torch.Tensor | None, tol: float, max_iters: int,
-              mode: PrecisionMode) -> tuple[SplitStack, SplitStack, DeviceReports]:
-    """NDB on split stacks (device-resident fast path used by the optimizer)."""
+              mode: PrecisionMode, complete: bool = True) -> tuple[SplitStack, SplitStack, DeviceReports]:
+    """NDB on split stacks (device-resident fast path used by the optimizer).
+
+    ``complete=False`` leaves Y and Z in upper pair-block storage (``dash_ndb_upper``); complete the one you
+    read with :func:`fill_lower`."""
     n, b = a.nmat, a.rows
     dev = a.data.device
     y, z = SplitStack(n, b, b, dev), SplitStack(n, b, b, dev)
     rep = DeviceReports(n, dev)
     L = _lib.lib()
     ws = workspace(L.dash_ndb_ws_bytes(n, b), dev)
-    st = L.dash_ndb(a.ref(), inv_scale.data_ptr() if inv_scale is not None else None, y.ref(), z.ref(),
-                    float(tol), int(max_iters), passes_for(mode), rep.iters.data_ptr(), rep.resid.data_ptr(),
-                    rep.conv.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+    fn = L.dash_ndb if complete else L.dash_ndb_upper
+    st = fn(a.ref(), inv_scale.data_ptr() if inv_scale is not None else None, y.ref(), z.ref(),
+            float(tol), int(max_iters), passes_for(mode), rep.iters.data_ptr(), rep.resid.data_ptr(),
+            rep.conv.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr())
     _lib.check(st, "dash_ndb")
     return y, z, rep
+
+
+def fill_lower(s: SplitStack) -> SplitStack:
+    """Complete an upper pair-block stored stack in place (``dash_fill_lower``)."""
+    _lib.check(_lib.lib().dash_fill_lower(s.ref(), _lib.stream_ptr()), "dash_fill_lower")
+    return s
 
 
 def cn_split(a: SplitStack, inv_scale: torch.Tensor | None, cfg: CnConfig,

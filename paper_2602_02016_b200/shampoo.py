@@ -31,7 +31,7 @@ from .chebyshev import ChebCoefficients, clenshaw_split, fit_inverse_root
 from .eigensolver import DampeningHeuristic, HeuristicKind, evd_inverse_root_torch
 from .errors import ConvergenceError, DegenerateSpectrumError
 from .linalg import PrecisionMode, SplitStack, device, format_matrix, parse_matrix, passes_for, workspace
-from .roots import CnConfig, DeviceReports, cn_split, ndb_split
+from .roots import CnConfig, DeviceReports, cn_split, fill_lower, ndb_split
 from .spectral import Frobenius, PowerIterationScaling, ScalingMode, block_seed, power_iteration_scales
 
 SOLVER_METHODS = ("evd", "cn", "ndb", "cbshv")
@@ -462,13 +462,16 @@ def refresh_inverse_roots(state: ShampooState, cfg: ShampooConfig, seed: int = 0
             reps = [rep]
             src = x
         else:  # ndb
+            # the iterates stay in upper pair-block storage; only the outputs read next are completed
             if p == 2:
-                _, src, rep = ndb_split(a, inv, solver.tolerance, solver.max_iters, mode)
+                _, src, rep = ndb_split(a, inv, solver.tolerance, solver.max_iters, mode, complete=False)
                 reps = [rep]
             else:
-                y1, _, r1 = ndb_split(a, inv, solver.tolerance, solver.max_iters, mode)
-                _, src, r2 = ndb_split(y1, None, solver.tolerance, solver.max_iters, mode)
+                y1, _, r1 = ndb_split(a, inv, solver.tolerance, solver.max_iters, mode, complete=False)
+                _, src, r2 = ndb_split(fill_lower(y1), None, solver.tolerance, solver.max_iters, mode,
+                                       complete=False)
                 reps = [r1, r2]
+            fill_lower(src)
         # roots = Z * scale^(-1/p)  -> fp32 state roots + split copy for the apply
         _lib.check(L.dash_scale_stack(src.ref(), inv.data_ptr(), 1.0 / p, group.roots.data_ptr(),
                                       group.roots.stride(0), group.roots.stride(1), rt.root_split[gi].ref(),

@@ -226,3 +226,20 @@ def test_power_iteration_tensor_cores_vs_oracle(d):
     np.testing.assert_allclose(sc.cpu().numpy(), want, rtol=2e-6)
     np.testing.assert_allclose(sc.cpu().numpy(), sc2.cpu().numpy(), rtol=2e-6)
     assert int(st.abs().sum()) == 0
+
+
+@pytest.mark.parametrize("b", [640, 1024])
+def test_ndb_upper_storage_fill_matches_complete(b):
+    """dash_ndb_upper + dash_fill_lower on the read output == dash_ndb (bitwise; ragged last pair block at 640)."""
+    import torch
+
+    from paper_2602_02016_b200.linalg import PrecisionMode, SplitStack
+
+    a = np.stack([core.random_spd(b, c, seed=30 + i, scale=0.5) for i, c in enumerate([10.0, 1e2])])
+    sa = SplitStack.from_float(torch.tensor(a, dtype=torch.float32, device="cuda"))
+    y, z, _ = roots.ndb_split(sa, None, 0.0, 8, PrecisionMode.EMULATED32)
+    yu, zu, _ = roots.ndb_split(sa, None, 0.0, 8, PrecisionMode.EMULATED32, complete=False)
+    assert torch.equal(z.to_float(), roots.fill_lower(zu).to_float())
+    assert torch.equal(y.to_float(), roots.fill_lower(yu).to_float())
+    zf = z.to_float().double()
+    assert float((zf - zf.transpose(1, 2)).abs().max()) < 1e-5 * float(zf.abs().max())
