@@ -423,7 +423,7 @@ int dash_unsplit(const dash_stack* src, float* dst, long long dst_mat_stride, in
   return unsplit_stack(*src, dst, dst_mat_stride, dst_ld, static_cast<cudaStream_t>(stream));
 }
 
-size_t dash_bmm_ws_bytes(int nmat) { return JobBuilder::bytes_for(8, nmat); }
+size_t dash_bmm_ws_bytes(int nmat) { return JobBuilder::bytes_for(16, nmat); }
 
 int dash_bmm(const dash_stack* a, int trans_a, const dash_stack* b, int trans_b, const dash_stack* c,
              float* f_out, long long f_mat_stride, int f_ld, float alpha, int passes, void* ws, size_t ws_bytes,

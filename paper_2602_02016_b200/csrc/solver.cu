@@ -381,7 +381,7 @@ int fill_lower(const dash_stack& s, cudaStream_t st) {
 // ---------------------------------------------------------------------------- NDB
 size_t ndb_ws_bytes(int n, int b) {  // NOLINT
   const size_t stacks = 3 * stack_bytes(n, b, b);
-  const size_t jobs = 4 * JobBuilder::bytes_for(8, 2 * n) + JobBuilder::bytes_for(8, n);
+  const size_t jobs = 4 * JobBuilder::bytes_for(32, 2 * n) + JobBuilder::bytes_for(32, n);
   return stacks + jobs + state_bytes(n) + 4096;
 }
 
@@ -495,7 +495,7 @@ int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_o
 // ---------------------------------------------------------------------------- Coupled Newton
 size_t cn_ws_bytes(int n, int b) {
   const size_t stacks = 6 * stack_bytes(n, b, b);
-  const size_t jobs = 2 * (3 * JobBuilder::bytes_for(8, 2 * n)) + JobBuilder::bytes_for(8, n) * 2;
+  const size_t jobs = 2 * (3 * JobBuilder::bytes_for(32, 2 * n)) + JobBuilder::bytes_for(32, n) * 2;
   return stacks + jobs + state_bytes(n) + Arena::need(4 * n) + 4096;
 }
 
@@ -650,7 +650,7 @@ __global__ void cheb_first_kernel(dash_stack a, const float* __restrict__ inv_sc
 }
 
 size_t cheb_ws_bytes(int n, int b) {
-  return 4 * stack_bytes(n, b, b) + 4 * JobBuilder::bytes_for(8, n) + Arena::need(4 * 1024) + 4096;
+  return 4 * stack_bytes(n, b, b) + 4 * JobBuilder::bytes_for(32, n) + Arena::need(4 * 1024) + 4096;
 }
 
 __global__ void pick_scalar_kernel(float* dst, const float* src, int k) { *dst = src[k]; }
@@ -672,7 +672,10 @@ int cheb_solve(const dash_stack& a, const float* inv_scale, const float* mult, c
   for (int k = 0; k <= degree; ++k) hc[k] = static_cast<float>(coeffs[k]);
   cudaMemcpyAsync(d_coef, hc.data(), sizeof(float) * hc.size(), cudaMemcpyHostToDevice, st);
   for (const dash_stack* t : std::initializer_list<const dash_stack*>{&sm, &bb[0], &bb[1], &bb[2]}) zero_padding(*t, st);
-  // rotation r holds the jobs for every k with k % 3 == r: B_k = 2 S B_{k+1} - B_{k+2} + c_k I
+  // rotation r holds the jobs for every k with k % 3 == r: B_k = 2 S B_{k+1} - B_{k+2} + c_k I.  The B_k are
+  // polynomials in S, stored as upper pair blocks (the side input is read only at stored positions); the
+  // final product reads B_1 that way and writes complete outputs.
+  const int up = ndb_upper_storage() ? 1 : 0;
   UploadedGemm g_rot[3], g_fin;
   for (int r = 0; r < 3; ++r) {
     JobBuilder jb;
@@ -682,6 +685,7 @@ int cheb_solve(const dash_stack& a, const float* inv_scale, const float* mult, c
       j.op = EPI_CHEB;
       j.out_mat = m;
       j.sym = 1;
+      j.b_up = j.c_up = up;
       j.gamma_p = cur;
       jb.set_side(j, bb[(r + 2) % 3], m);
       jb.set_out(j, bb[r], m);
@@ -697,6 +701,7 @@ int cheb_solve(const dash_stack& a, const float* inv_scale, const float* mult, c
       j.op = EPI_CHEB_FINAL;
       j.out_mat = m;
       j.sym = 1;
+      j.b_up = up;
       j.gamma = hc[0];
       j.alpha_p = mult;
       jb.set_side(j, bb[2], m);

@@ -1,6 +1,3 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
-run() { env "$@" DASH_GEMM_DEBUG=2 timeout 300 python tools/solver_bench.py --n 256 --b 1024 --iters 10 --mode f32 --reps 2 2>&1 | grep "\[gemm\].*10240" | sort | uniq -c | sort -rn | head -1; env "$@" timeout 300 python tools/solver_bench.py --n 256 --b 1024 --iters 10 --mode f32 | grep "ndb"; }
-for u in 0 1 0 1; do echo "== up $u"; run DASH_NDB_UP=$u; done
-echo "== up f16"; timeout 300 python tools/solver_bench.py --n 256 --b 1024 --iters 10 --mode f16 | grep "ndb: total"
-echo "== noup f16"; DASH_NDB_UP=0 timeout 300 python tools/solver_bench.py --n 256 --b 1024 --iters 10 --mode f16 | grep "ndb: total"
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+for u in 0 1; do for pr in f32 f16; do echo "== up $u $pr"; DASH_NDB_UP=$u timeout 600 python bench.py --solver cbshv --precision $pr --no-cpu --no-e2e --steps 3 --warmup 3 2>/dev/null | python3 -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['value'], d['clocks']['sm_mhz'], d['roofline']['achieved'], d['phases_ms'])"; done; done
