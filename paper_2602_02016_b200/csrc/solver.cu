@@ -519,6 +519,7 @@ int cn_solve(const dash_stack& a, const float* inv_scale, int p, float c, const 
   if (!ar.ok) return DASH_EINVAL;
   const dash_stack xs[2] = {x_out, x2};
   const dash_stack ms[2] = {m1, m2};
+  const int up = ndb_upper_storage() ? 1 : 0;  // X, M, C are polynomials in a: upper pair-block storage
   UploadedGemm g_xc[2], g_c4, g_m[2];
   for (int par = 0; par < 2; ++par) {
     JobBuilder j1;  // X' = X C and C2 = C C in one launch
@@ -526,10 +527,12 @@ int cn_solve(const dash_stack& a, const float* inv_scale, int p, float c, const 
       GemmJob j;
       if (!j1.operands(j, xs[par], m, 0, corr, m, kSymB)) return DASH_EINVAL;
       j.op = EPI_SPLIT; j.out_mat = m; j.sym = 1;
+      j.a_up = j.b_up = j.c_up = up;
       j1.set_out(j, xs[par ^ 1], m);
       j1.push(j);
       if (!j1.operands(j, corr, m, 0, corr, m, kSymB)) return DASH_EINVAL;
       j.op = EPI_SPLIT; j.out_mat = m; j.sym = 1;
+      j.a_up = j.b_up = j.c_up = up;
       j1.set_out(j, cp, m);
       j1.push(j);
     }
@@ -540,6 +543,7 @@ int cn_solve(const dash_stack& a, const float* inv_scale, int p, float c, const 
       GemmJob j;
       if (!j3.operands(j, cpow, m, 0, ms[par], m, kSymB)) return DASH_EINVAL;
       j.op = EPI_CN_M; j.out_mat = m; j.sym = 1;
+      j.a_up = j.b_up = j.c_up = up;
       j.beta = static_cast<float>(p);
       j.active = s.active;
       j.resid = s.resid;
@@ -555,6 +559,7 @@ int cn_solve(const dash_stack& a, const float* inv_scale, int p, float c, const 
       GemmJob j;
       if (!j2.operands(j, cp, m, 0, cp, m, kSymB)) return DASH_EINVAL;
       j.op = EPI_SPLIT; j.out_mat = m; j.sym = 1;
+      j.a_up = j.b_up = j.c_up = up;
       j2.set_out(j, c4, m);
       j2.push(j);
     }
@@ -589,6 +594,7 @@ int cn_solve(const dash_stack& a, const float* inv_scale, int p, float c, const 
   finish_kernel<<<(n + 255) / 256, 256, 0, st>>>(s, n, max_iters, iters, resid_out, conv);
   note_launch();
   copy_stack_if(s.par, 1, x_out, x2, st);
+  if (up) fill_lower(x_out, st);
   if (products) *products = np;
   return cuda_ok();
 }
