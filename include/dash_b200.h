@@ -92,7 +92,8 @@ int dash_ndb(const dash_stack* a, const float* inv_scale, const dash_stack* y, c
  *   p in {2, 4}, c = CnConfig.resolved_c (roots.py:53-56). */
 /* dash_ndb_upper: dash_ndb leaving y and z in upper pair-block storage (only the 256x256 blocks on or above
  *   the block diagonal are valid, diagonal blocks complete) -- the optimizer completes only the
- *   output it reads.  dash_fill_lower completes such a stack in place (lower blocks <- transposed upper);
+ *   output it reads; the input a may itself be upper-stored (dash_ndb accepts that too).  dash_fill_lower
+ *   completes such a stack in place (lower blocks <- transposed upper);
  *   both are plain dash_ndb / a no-op when the iterates are stored complete (DASH_NDB_UP=0, DASH_KB=32). */
 int dash_ndb_upper(const dash_stack* a, const float* inv_scale, const dash_stack* y, const dash_stack* z, float tol,
                    int max_iters, int passes, int* iters, float* resid, int* conv, void* ws, size_t ws_bytes,

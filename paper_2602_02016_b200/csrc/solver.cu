@@ -143,8 +143,10 @@ __global__ void finish_kernel(BlockState s, int n, int max_iters, int* iters, fl
 // ---------------------------------------------------------------------------- elementwise kernels
 // NDB closed-form first iteration (roots.py:267-271): E1 = 1.5 I - 0.5 a_hat, Z1 = E1,
 // residual max|E1 - I|; a_hat = a * inv_scale[m].
+// upper = 1: E1 / Z1 are consumed only as upper pair-block operands, so only those blocks of `a` are read
+// and written (the input may itself be upper-stored, e.g. the first solve's Y of an inverse 4th root).
 __global__ void ndb_first_kernel(dash_stack a, const float* __restrict__ inv_scale, dash_stack e, dash_stack z,
-                                 unsigned* __restrict__ resid) {
+                                 unsigned* __restrict__ resid, int upper) {
   const int m = blockIdx.y;
   const int n = a.rows;
   const float sa = ldexpf(1.f, a.exp[m]) * (inv_scale ? inv_scale[m] : 1.f);
@@ -155,6 +157,7 @@ __global__ void ndb_first_kernel(dash_stack a, const float* __restrict__ inv_sca
   float rmax = 0.f, amax = 0.f;
   bool ovf = false;
   for_chunks8(n, a.ld, [&](int r, int c) {
+    if (upper && (r >> 8) > (c >> 8)) return;  // lower pair block (never read)
     float v[8];
     load_split8(ah, mat_plane(a), static_cast<long long>(r) * a.ld + c, sa, v);
 #pragma unroll
@@ -408,7 +411,7 @@ int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_o
       j.op = EPI_SPLIT;
       j.out_mat = m;
       j.sym = 1;
-      j.c_up = up;
+      j.a_up = j.b_up = j.c_up = up;  // a may itself be upper-stored; E1 is
       j.alpha_p = inv_scale;
       jb.set_out(j, ys[1], m);
       jb.push(j);
@@ -461,7 +464,7 @@ int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_o
   cudaMemsetAsync(e.amax, 0, sizeof(unsigned) * n, st);
   cudaMemsetAsync(z2.amax, 0, sizeof(unsigned) * n, st);
   cudaMemsetAsync(y2.amax, 0, sizeof(unsigned) * n, st);
-  ndb_first_kernel<<<egrid(a), 256, 0, st>>>(a, inv_scale, e, z2, s.resid);
+  ndb_first_kernel<<<egrid(a), 256, 0, st>>>(a, inv_scale, e, z2, s.resid, up);
   note_launch();
   if (int rc = g_first.run(passes, st)) return rc;
   ++np;

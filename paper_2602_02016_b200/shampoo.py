@@ -462,14 +462,14 @@ def refresh_inverse_roots(state: ShampooState, cfg: ShampooConfig, seed: int = 0
             reps = [rep]
             src = x
         else:  # ndb
-            # the iterates stay in upper pair-block storage; only the outputs read next are completed
+            # the iterates stay in upper pair-block storage (the second solve of a 4th root reads Y1 that way);
+            # only the root that is read next is completed
             if p == 2:
                 _, src, rep = ndb_split(a, inv, solver.tolerance, solver.max_iters, mode, complete=False)
                 reps = [rep]
             else:
                 y1, _, r1 = ndb_split(a, inv, solver.tolerance, solver.max_iters, mode, complete=False)
-                _, src, r2 = ndb_split(fill_lower(y1), None, solver.tolerance, solver.max_iters, mode,
-                                       complete=False)
+                _, src, r2 = ndb_split(y1, None, solver.tolerance, solver.max_iters, mode, complete=False)
                 reps = [r1, r2]
             fill_lower(src)
         # roots = Z * scale^(-1/p)  -> fp32 state roots + split copy for the apply

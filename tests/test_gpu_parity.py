@@ -243,3 +243,18 @@ def test_ndb_upper_storage_fill_matches_complete(b):
     assert torch.equal(y.to_float(), roots.fill_lower(yu).to_float())
     zf = z.to_float().double()
     assert float((zf - zf.transpose(1, 2)).abs().max()) < 1e-5 * float(zf.abs().max())
+
+
+def test_ndb_chain_reads_upper_stored_input():
+    """Inverse 4th root chain: the second solve on the upper-stored Y1 == on the completed Y1 (bitwise)."""
+    import torch
+
+    from paper_2602_02016_b200.linalg import PrecisionMode, SplitStack
+
+    a = np.stack([core.random_spd(768, c, seed=40 + i, scale=0.5) for i, c in enumerate([10.0, 1e2])])
+    sa = SplitStack.from_float(torch.tensor(a, dtype=torch.float32, device="cuda"))
+    y1u, _, _ = roots.ndb_split(sa, None, 0.0, 6, PrecisionMode.EMULATED32, complete=False)
+    y1, _, _ = roots.ndb_split(sa, None, 0.0, 6, PrecisionMode.EMULATED32)
+    _, zu, _ = roots.ndb_split(y1u, None, 0.0, 6, PrecisionMode.EMULATED32, complete=False)
+    _, z, _ = roots.ndb_split(y1, None, 0.0, 6, PrecisionMode.EMULATED32)
+    assert torch.equal(z.to_float(), roots.fill_lower(zu).to_float())
