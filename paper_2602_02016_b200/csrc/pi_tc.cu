@@ -125,18 +125,30 @@ __device__ __forceinline__ uint32_t pt_v_off(int n, int k, int p) {
 // valid in lanes 0..15 of row warp 0 (lane j holds column j).
 __device__ __forceinline__ double pt_cta_colsum(const float (&w)[kPtPool], double* wpart, int rw, int lane) {
   rows_sync();  // previous users of wpart are done
+  // transpose-reduce: at offset o the lane pair (l, l ^ o) splits its remaining columns in halves, each lane
+  // keeps one half and adds the partner's copy of it (16 + 8 + 4 + 2 + 1 values; fixed order)
+  double t[kPtPool];
 #pragma unroll
-  for (int j = 0; j < kPtPool; ++j) {
-    double t = static_cast<double>(w[j]) * w[j];
+  for (int j = 0; j < kPtPool; ++j) t[j] = static_cast<double>(w[j]) * w[j];
+  int col = 0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    if (lane == 0) wpart[rw * kPtPool + j] = t;
+  for (int o = 16, n = kPtPool / 2; o > 1; o >>= 1, n >>= 1) {
+    const bool hi = (lane & o) != 0;
+#pragma unroll
+    for (int j = 0; j < n; ++j) {
+      const double send = hi ? t[j] : t[j + n];
+      const double keep = hi ? t[j + n] : t[j];
+      t[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+    col += hi ? n : 0;
   }
+  t[0] += __shfl_xor_sync(0xffffffffu, t[0], 1);  // lanes l, l ^ 1 now both hold column `col`
+  if ((lane & 1) == 0) wpart[rw * kPtPool + col] = t[0];
   rows_sync();
-  double t = 0.0;
+  double sum = 0.0;
   if (rw == 0 && lane < kPtPool)
-    for (int w4 = 0; w4 < 4; ++w4) t += wpart[w4 * kPtPool + lane];
-  return t;
+    for (int w4 = 0; w4 < 4; ++w4) sum += wpart[w4 * kPtPool + lane];
+  return sum;
 }
 
 __global__ void __launch_bounds__(kPtThreads, 1)
@@ -263,7 +275,10 @@ __global__ void __launch_bounds__(kPtThreads, 1)
     const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16);
     const float sa = ldexpf(1.f, __ldg(a.exp + m) + kVExp);
     float amax_a = __uint_as_float(__ldg(a.amax + m));
-    const double sfix = amax_a > 0.f ? sqrt(static_cast<double>(d)) * amax_a : 1.0;  // |W_i| <= |a_i|_2 <= sfix
+    // |W_i| <= |a_i|_2 <= sqrt(d) max|a| <= sfix, a power of two: the stored pool W / sfix is an exact scaling
+    const double sfix =
+        amax_a > 0.f ? ldexp(1.0, ilogb(sqrt(static_cast<double>(d)) * static_cast<double>(amax_a)) + 1) : 1.0;
+    const float inv_sfix = static_cast<float>(1.0 / sfix);
     uint64_t bseed = rng::block_seed(seed, static_cast<uint64_t>(seed_index ? seed_index[m] : m));
     const uint32_t vbar_peer0 = smem_u32(vbar);
     const uint32_t my_slice = static_cast<uint32_t>(row0 / 64) * kPtVkb;  // my 2 k-blocks (8 KB) of a pool buffer
@@ -344,12 +359,16 @@ __global__ void __launch_bounds__(kPtThreads, 1)
         vphase ^= 1;
         if (it > 0) {
           const double* pp = pn + ((ex - 1) & 1) * 8 * kPtPool;
+          float fl = 0.f;  // lane j < 16: the scale of pool column j, then broadcast
+          if (lane < kPtPool) {
+            double nsq = 0.0;
+            for (int r = 0; r < C; ++r) nsq += pp[r * kPtPool + lane];  // ranks in order
+            const double nn = sqrt(nsq);
+            fl = nn > 0.0 ? static_cast<float>(sfix / nn) : 0.f;
+          }
 #pragma unroll
           for (int j = 0; j < kPtPool; ++j) {
-            double nsq = 0.0;
-            for (int r = 0; r < C; ++r) nsq += pp[r * kPtPool + j];  // ranks in order
-            const double nn = sqrt(nsq);
-            f[j] = nn > 0.0 ? static_cast<float>(sfix / nn) : 0.f;
+            f[j] = __shfl_sync(0xffffffffu, fl, j);
             v[j] = vs[j] * f[j];
           }
         }
@@ -366,7 +385,7 @@ __global__ void __launch_bounds__(kPtThreads, 1)
         if (it < iters) {
           const double partial = pt_cta_colsum(w, wpart, rw, static_cast<int>(lane));
 #pragma unroll
-          for (int j = 0; j < kPtPool; ++j) vs[j] = static_cast<float>(static_cast<double>(w[j]) / sfix);
+          for (int j = 0; j < kPtPool; ++j) vs[j] = w[j] * inv_sfix;  // exact (power-of-two scale)
           publish(partial);
         } else {
 #pragma unroll
