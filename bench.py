@@ -122,41 +122,155 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU baseline (oracle port)
-def cpu_baseline(shapes, bsz, iters, budget_s: float = 20.0, method: str = "ndb"):
-    """Time the float64 oracle (restatement of the reference step) on a bounded sample and extrapolate."""
+def _host_threads() -> int:
+    return min(len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1), 64)
+
+
+def cpu_baseline(shapes, bsz, iters, method: str = "ndb", blocks_per_group: int = 1, reps: int = 3):
+    """The reference algorithm (float64 oracle restatement) on the host cores, measured per component.
+
+    * every distinct gradient-block shape (r, c) (and 1-D chunk length): one optimizer step of a layer of exactly
+      that shape with the refresh skipped -- statistics EMA, Adam, the U = L^(-1/4) G R^(-1/4) apply and the grafted
+      update (shampoo.py:238-278, :380-403) -- times the number of such blocks in the workload (the per-layer work
+      is a sum over its blocks plus elementwise passes over its elements, so this is exact up to loop overhead);
+    * every (dim, p) preconditioner group: the refresh of `blocks_per_group` blocks (a = ema + eps I, pooled
+      power iteration 16 x 30, the solver at the bench's settings, the rescale; shampoo.py:312-349), times the
+      group size / sample size (fixed-iteration solver cost does not depend on the values).
+    BLAS runs on every host thread available (scipy-openblas caps at 64).  Each component is the median of
+    `reps` timings."""
+    import threadpoolctl
+
+    from oracle import core
+    from paper_2602_02016_b200.shampoo import build_layout
+
+    threads = _host_threads()
+    t_start = time.perf_counter()
+    rng = np.random.default_rng(0)
+    cfg = core.OracleConfig(block_size=bsz, method=method, tolerance=0.0, max_iters=iters, update_freq=2)
+    layers, specs = build_layout(shapes, bsz)
+    counts: dict = {}
+    for lay in layers:
+        if lay.is_matrix:
+            for (r0, r1), (c0, c1) in lay.layout.block_spans:
+                counts[(r1 - r0, c1 - c0)] = counts.get((r1 - r0, c1 - c0), 0) + 1
+        else:
+            for s0, e0 in lay.chunk_bounds:
+                counts[(e0 - s0,)] = counts.get((e0 - s0,), 0) + 1
+    parts = {}
+
+    def timed(fn):
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+        return statistics.median(ts)
+
+    with threadpoolctl.threadpool_limits(threads):
+        layer_ms = 0.0
+        for shp, cnt in sorted(counts.items()):
+            theta = rng.standard_normal(shp) * 0.02
+            grad = rng.standard_normal(shp) * 1e-3
+
+            def one_block():
+                st = core.init_state([theta], cfg)
+                st["step"] = 1  # 1 % update_freq(2) != 0: statistics + apply only
+                core.step(st, [theta], [grad], cfg, seed=0)
+
+            dt = timed(one_block)
+            layer_ms += dt * cnt * 1e3
+            parts[f"block{shp}"] = {"ms_each": round(dt * 1e3, 2), "count": cnt}
+        group_ms = 0.0
+        for gi, g in enumerate(specs):
+            k = min(blocks_per_group, len(g.members))
+            x = rng.standard_normal((k, g.dim, g.dim + 8)) * 1e-3
+            ema = np.einsum("nij,nkj->nik", x, x) * 0.05
+
+            def refresh_sample():
+                a = ema + cfg.epsilon * np.eye(g.dim)
+                sc = core.group_scales(a, "pi", 16, 30, core.block_seed(7, gi))
+                ahat = a / sc[:, None, None]
+                if method == "ndb":
+                    if g.exponent == 2:
+                        _, roots, _ = core.batched_newton_db(ahat, 0.0, iters)
+                    else:
+                        y1, _, _ = core.batched_newton_db(ahat, 0.0, iters)
+                        _, roots, _ = core.batched_newton_db(y1, 0.0, iters)
+                elif method == "cn":
+                    roots, _ = core.batched_coupled_newton(ahat, g.exponent, 0.0, iters)
+                else:
+                    coeffs, _ = core.cheb_coefficients(g.exponent, 60, 1000, None)
+                    roots = core.batched_clenshaw(a, coeffs, sc, g.exponent)
+                return roots * np.power(sc, -1.0 / g.exponent)[:, None, None]
+
+            dt = timed(refresh_sample)
+            group_ms += dt / k * len(g.members) * 1e3
+            parts[f"group{g.dim}/p{g.exponent}"] = {"ms_per_block": round(dt / k * 1e3, 1), "blocks": len(g.members),
+                                                    "sampled": k}
+    wall = time.perf_counter() - t_start
+    return {
+        "value": round(layer_ms + group_ms, 1),
+        "unit": "ms",
+        "cores": threads,
+        "nproc": os.cpu_count(),
+        "blas_threads": threads,
+        "kind": "port",
+        "sample": (f"float64 oracle of the reference step, timed per component on this host ({threads} BLAS threads): "
+                   f"statistics + apply + graft of one block of every distinct block shape x its count, and the "
+                   f"refresh (PI 16x30 + {SOLVER_DESC[method].format(k=iters)}) of {blocks_per_group} block(s) per "
+                   f"(dim, p) group x group size; measured in {wall:.1f} s (not extrapolated by FLOPs)"),
+        "components_ms": {"stats_apply": round(layer_ms, 1), "refresh": round(group_ms, 1)},
+        "parts": parts,
+    }
+
+
+def c1_pair(iters: int, with_gpu: bool = True) -> dict:
+    """Config 1 (one 1024x1024 layer, B = 256, NDB fixed `iters`, PI) end to end on both sides: the reference
+    algorithm (float64 oracle, all host threads) runs it in full, so this ratio is same-config and unextrapolated."""
     import threadpoolctl
 
     from oracle import core
 
-    sample_shapes = [(2048, 2048)]
     rng = np.random.default_rng(0)
-    params = [rng.standard_normal(s) * 0.02 for s in sample_shapes]
-    grads = [rng.standard_normal(s) * 1e-3 for s in sample_shapes]
-    cfg = core.OracleConfig(block_size=bsz, method=method, tolerance=0.0, max_iters=iters)
-    times = []
-    t_start = time.perf_counter()
-    while True:
-        st = core.init_state(params, cfg)
-        t0 = time.perf_counter()
-        core.step(st, params, grads, cfg, seed=0)
-        times.append(time.perf_counter() - t0)
-        if time.perf_counter() - t_start > budget_s * 0.5 or len(times) >= 5:
-            break
-    t = statistics.median(times)
-    full = solver_flops(shapes, bsz, iters, method)
-    samp = solver_flops(sample_shapes, bsz, iters, method)
-    scale = sum(full.values()) / sum(samp.values())
-    info = threadpoolctl.threadpool_info()
-    cores = max([i.get("num_threads", 1) for i in info] + [1])
-    return {
-        "value": t * scale * 1e3,
-        "unit": "ms",
-        "cores": cores,
-        "kind": "port",
-        "sample": (f"oracle float64 step on one (2048,2048) layer (8 blocks of 1024, "
-                   f"{SOLVER_DESC[method].format(k=iters)}, PI 16x30), median {len(times)} runs = {t:.2f} s, "
-                   f"extrapolated x{scale:.1f} by algorithmic FLOPs"),
-    }
+    w = rng.standard_normal((1024, 1024))
+    g = rng.standard_normal((1024, 1024))
+    ocfg = core.OracleConfig(block_size=256, method="ndb", tolerance=0.0, max_iters=iters)
+    with threadpoolctl.threadpool_limits(_host_threads()):
+        times = []
+        for _ in range(3):
+            ost = core.init_state([w], ocfg)
+            t0 = time.perf_counter()
+            oout, _, _ = core.step(ost, [w], [g], ocfg, seed=0)
+            times.append(time.perf_counter() - t0)
+    res = {"workload": f"c1: one (1024,1024) layer, B=256, NDB fixed {iters} iters/chain, PI 16x30, one step",
+           "reference_ms": round(statistics.median(times) * 1e3, 1), "reference_threads": _host_threads()}
+    if with_gpu:
+        import torch
+
+        from paper_2602_02016_b200.shampoo import ShampooConfig, SolverConfig, init_state, step
+
+        cfg = ShampooConfig(block_size=256, solver=SolverConfig(method="ndb", tolerance=0.0, max_iters=iters))
+        hw = torch.from_numpy(w.astype(np.float32)).pin_memory()
+        hg = torch.from_numpy(g.astype(np.float32)).pin_memory()
+        st = init_state([hw], cfg)
+        for _ in range(3):
+            st = init_state([hw], cfg)
+            step(st, [hw], [hg], cfg, seed=0)
+        torch.cuda.synchronize()
+        e2e = []
+        for _ in range(5):
+            st = init_state([hw], cfg)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            out, _ = step(st, [hw], [hg], cfg, seed=0)
+            torch.cuda.synchronize()
+            e2e.append(time.perf_counter() - t0)
+        d = (out[0].double().numpy() - w)
+        ref = oout[0] - w
+        res["dash_e2e_ms"] = round(statistics.median(e2e) * 1e3, 3)
+        res["ratio_reference_over_dash_e2e"] = round(res["reference_ms"] / res["dash_e2e_ms"], 1)
+        res["parity_update_relF"] = float(np.linalg.norm(d - ref) / np.linalg.norm(ref))
+    return res
 
 
 # ----------------------------------------------------------------------------- DASH arm

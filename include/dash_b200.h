@@ -81,12 +81,15 @@ int dash_bmm(const dash_stack* a, int trans_a, const dash_stack* b, int trans_b,
  * (inv_scale may be NULL = 1), i.e. the reference's a / scales (shampoo.py:326).  Per-block reports are
  * written to device arrays iters[N], resid[N] (float), conv[N] (0/1) exactly as IterationReport
  * (roots.py:32-36).  tol = 0 is fixed-iteration mode.  passes: 3 = split-f16 (fp32-class), 1 = fp16.
+ * stall > 0 (used when the requested tolerance is below the rounding floor of the arithmetic): a block whose
+ * residual stops decreasing (r_k >= r_{k-1}) once r_{k-1} <= stall is frozen as converged at that floor;
+ * stall = 0 keeps the reference's rules exactly (non-finite, r <= tol, divergence watch).
  *
  * dash_ndb: batched Newton-Denman-Beavers (roots.batched_newton_db, roots.py:262-305):
  *   y <- a_hat^(1/2), z <- a_hat^(-1/2). */
 size_t dash_ndb_ws_bytes(int n, int b);
 int dash_ndb(const dash_stack* a, const float* inv_scale, const dash_stack* y, const dash_stack* z, float tol,
-             int max_iters, int passes, int* iters, float* resid, int* conv, void* ws, size_t ws_bytes,
+             float stall, int max_iters, int passes, int* iters, float* resid, int* conv, void* ws, size_t ws_bytes,
              void* stream);
 /* dash_cn: batched coupled Newton (roots.batched_coupled_newton, roots.py:216-259): x <- a_hat^(-1/p),
  *   p in {2, 4}, c = CnConfig.resolved_c (roots.py:53-56). */
@@ -96,23 +99,32 @@ int dash_ndb(const dash_stack* a, const float* inv_scale, const dash_stack* y, c
  *   completes such a stack in place (lower blocks <- transposed upper);
  *   both are plain dash_ndb / a no-op when the iterates are stored complete (DASH_NDB_UP=0, DASH_KB=32). */
 int dash_ndb_upper(const dash_stack* a, const float* inv_scale, const dash_stack* y, const dash_stack* z, float tol,
-                   int max_iters, int passes, int* iters, float* resid, int* conv, void* ws, size_t ws_bytes,
+                   float stall, int max_iters, int passes, int* iters, float* resid, int* conv, void* ws, size_t ws_bytes,
                    void* stream);
 int dash_fill_lower(const dash_stack* s, void* stream);
 size_t dash_cn_ws_bytes(int n, int b);
 int dash_cn(const dash_stack* a, const float* inv_scale, int p, float c, const dash_stack* x, float tol,
-            int max_iters, int passes, int* iters, float* resid, int* conv, void* ws, size_t ws_bytes,
+            float stall, int max_iters, int passes, int* iters, float* resid, int* conv, void* ws, size_t ws_bytes,
             void* stream);
 /* dash_scale_stack: v = value * mult[m]^pw -> fp32 f_out and/or split dst (the root rescale
- *   roots * scales^(-1/p), shampoo.py:348, with mult = 1/scale and pw = 1/p). */
+ *   roots * scales^(-1/p), shampoo.py:348, with mult = 1/scale and pw = 1/p).  gate (device int, may be
+ *   NULL): nothing is written unless *gate != 0 (a group that failed its scale checks keeps its roots). */
 int dash_scale_stack(const dash_stack* src, const float* mult, float pw, float* f_out, long long f_mat_stride,
-                     int f_ld, const dash_stack* dst, void* stream);
+                     int f_ld, const dash_stack* dst, const int* gate, void* stream);
+/* dash_scale_check: the refresh's scale checks for one group, on the device (shampoo.py:324-325,
+ *   spectral.py:99-107): status[m] == 2 (pool collapsed twice) -> code 2 (DegenerateSpectrumError), a
+ *   non-positive / non-finite scale[m] -> code 1 (ConvergenceError).  err[2] is shared by the groups of one
+ *   refresh (zeroed by the caller): the first failing group stores (code, group); *ok = 1 iff no group failed
+ *   so far (the commit gate of dash_scale_stack / dash_clenshaw).  status may be NULL (Frobenius). */
+int dash_scale_check(const float* scale, const int* status, int n, int group, int* ok, int* err, void* stream);
 /* dash_clenshaw: optimized matrix Clenshaw of a Chebyshev series (chebyshev.batched_clenshaw_matrix,
  *   chebyshev.py:137-184) on S = 2 a inv_scale - I with coefficients coeffs[0..degree] (fit on the host,
- *   chebyshev.py:46-84), result * mult[m] -> fp32 f_out ([m][B][B]) and/or split out.  d-1 products. */
+ *   chebyshev.py:46-84), result * mult[m] -> fp32 f_out ([m][B][B]) and/or split out.  d-1 products.
+ *   gate (may be NULL): the final product writes the outputs only when *gate != 0. */
 size_t dash_cheb_ws_bytes(int n, int b);
 int dash_clenshaw(const dash_stack* a, const float* inv_scale, const float* mult, const double* coeffs, int degree,
-                  float* f_out, const dash_stack* out, int passes, void* ws, size_t ws_bytes, void* stream);
+                  float* f_out, const dash_stack* out, int passes, const int* gate, void* ws, size_t ws_bytes,
+                  void* stream);
 
 /* ---------------------------------------------------------------- optimizer step (shampoo.py)
  * dash_plan_create: register the block table (matrix blocks first, then 1-D chunks), the groups'
@@ -142,12 +154,15 @@ int dash_plan_apply(dash_plan* p, const float* theta_in, float* theta_out, float
  * max|a| / sum(a^2) partials of a = ema + eps I; split a; Frobenius scale; pooled power iteration
  * (spectral.py:87-117, block seeds block_seed(seed, i), NumPy-identical start vectors).
  * status[i]: 0 ok, 1 non-positive scale, 2 pool collapsed twice.  seed_index (device, nullable): global
- * block index used for block i's child seed (block sharding keeps the 1-GPU pools). */
+ * block index used for block i's child seed (block sharding keeps the 1-GPU pools).  vec_out (device,
+ * nullable, [n][d]): the selected normalized pool vector (spectral.py:108-112); a zero matrix gives
+ * lambda = 0 and its first start vector (spectral.py:99-101). */
 int dash_group_sym(float* ema, int n, int d, float eps, uint32_t* amax, float* fro_part, void* stream);
 int dash_group_split_a(const float* ema, float eps, const dash_stack* a, void* stream);
 int dash_fro_scale(const float* fro_part, int n, float* scale, float* inv_scale, void* stream);
 int dash_power_iteration(const float* ema, int n, int d, float eps, int pool, int iters, unsigned long long seed,
-                         float* scale, float* inv_scale, int* status, const int* seed_index, void* stream);
+                         float* scale, float* inv_scale, int* status, const int* seed_index, float* vec_out,
+                         void* stream);
 /* Same result from the solver's split stack a = ema + eps I (d a multiple of 128, <= 1024): tensor-core
  * matvecs (tcgen05, one d/128-CTA cluster per block, pool in shared memory).  Replaces the inner loop of
  * spectral.multi_power_iteration (spectral.py:77-112) for the DASH block sizes. */

@@ -37,6 +37,8 @@ class OracleConfig:
     lr_base: float = 1e-3
     lr_total: int = 0
     lr_final: float = 0.0
+    heuristic: str = "relu"          # EVD dampening: legacy | relu | abs (eigensolver.py:31-44)
+    heuristic_eps: float = 1e-10
 
     def lr(self, t: int) -> float:
         """LrSchedule.value (shampoo.py:103-109)."""
@@ -184,21 +186,24 @@ def _power_pool(a, v, iters):
 RETRY_SALT = 0x5EED  # spectral.py:50
 
 
-def multi_power_iteration(a, pool, iters, seed):
-    """Best Rayleigh quotient over the pool, one reseeded retry (spectral.py:87-112). Returns lambda."""
+def multi_power_iteration(a, pool, iters, seed, return_vector=False):
+    """Best Rayleigh quotient over the pool, one reseeded retry (spectral.py:87-112). Returns lambda
+    (and the selected unit vector with return_vector=True)."""
     n = a.shape[0]
-    v, q = _power_pool(a, start_vectors(n, pool, seed), iters)
+    v0 = start_vectors(n, pool, seed)
+    v, q = _power_pool(a, v0, iters)
     alive = np.linalg.norm(v, axis=0) > 0.0
     if not alive.any() or q[alive].max() == 0.0:
         if np.linalg.norm(a) == 0.0:
-            return 0.0
+            return (0.0, v0[:, 0]) if return_vector else 0.0
         v, q = _power_pool(a, start_vectors(n, pool, block_seed(seed, RETRY_SALT)), iters)
         alive = np.linalg.norm(v, axis=0) > 0.0
         if not alive.any() or q[alive].max() == 0.0:
             raise ArithmeticError("power iteration pool collapsed twice")
     best = int(np.argmax(np.where(alive, q, -np.inf)))
     x = v[:, best] / np.linalg.norm(v[:, best])
-    return float(x @ (a @ x)) / float(x @ x)
+    lam = float(x @ (a @ x)) / float(x @ x)
+    return (lam, x) if return_vector else lam
 
 
 def group_scales(a, scaling, pool, iters, seed):
@@ -355,7 +360,9 @@ def refresh(state, cfg: OracleConfig, seed=0):
     for gi, grp in enumerate(state["groups"]):
         p, n = grp["p"], grp["dim"]
         if cfg.method == "evd":
-            raise NotImplementedError("EVD comparator: use numpy eigh in tests")
+            grp["roots"] = evd_inverse_root(grp["ema"], p, cfg.heuristic, cfg.heuristic_eps)
+            all_reports.append(())
+            continue
         a = grp["ema"] + cfg.epsilon * np.eye(n)
         sc = group_scales(a, cfg.scaling, cfg.pool, cfg.pi_iters, block_seed(seed, gi))
         if (sc <= 0).any():
@@ -382,6 +389,24 @@ def refresh(state, cfg: OracleConfig, seed=0):
             continue
         grp["roots"] = roots * np.power(sc, -1.0 / p)[:, None, None]
     return all_reports
+
+
+def evd_inverse_root(ema, p, heuristic="relu", eps=1e-10):
+    """Batched EVD inverse root of ema + eps I with the LEGACY / SHIFTED_RELU / ABS spectrum heuristics
+    (eigensolver.py:133-179); numpy's eigh stands in for the reference's cyclic Jacobi (both converge to the
+    float64 eigendecomposition)."""
+    n = ema.shape[-1]
+    lam, q = np.linalg.eigh(ema + eps * np.eye(n))
+    if heuristic == "legacy":
+        proc = lam - np.minimum(lam.min(axis=-1, keepdims=True), 0.0) + eps
+    elif heuristic == "relu":
+        proc = np.maximum(lam - eps - eps, 0.0)
+    else:
+        proc = np.abs(lam - eps) + eps
+    if (~(proc > 0).any(axis=-1)).any():
+        raise ArithmeticError("all eigenvalues removed by dampening heuristic")
+    inv = np.where(proc > 0, np.power(np.where(proc > 0, proc, 1.0), -1.0 / p), 0.0)
+    return (q * inv[..., None, :]) @ np.swapaxes(q, -1, -2)
 
 
 def graft_scale(u, p):

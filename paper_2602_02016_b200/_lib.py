@@ -58,18 +58,19 @@ _SIGNATURES: dict[str, tuple] = {
     "dash_bmm": (c_int, [_P, c_int, _P, c_int, _P, c_void_p, c_longlong, c_int, c_float, c_int, c_void_p,
                          c_size_t, c_void_p]),
     "dash_ndb_ws_bytes": (c_size_t, [c_int, c_int]),
-    "dash_ndb": (c_int, [_P, c_void_p, _P, _P, c_float, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
-                         c_size_t, c_void_p]),
-    "dash_ndb_upper": (c_int, [_P, c_void_p, _P, _P, c_float, c_int, c_int, c_void_p, c_void_p, c_void_p,
+    "dash_ndb": (c_int, [_P, c_void_p, _P, _P, c_float, c_float, c_int, c_int, c_void_p, c_void_p, c_void_p,
+                         c_void_p, c_size_t, c_void_p]),
+    "dash_ndb_upper": (c_int, [_P, c_void_p, _P, _P, c_float, c_float, c_int, c_int, c_void_p, c_void_p, c_void_p,
                                c_void_p, c_size_t, c_void_p]),
     "dash_fill_lower": (c_int, [_P, c_void_p]),
     "dash_cn_ws_bytes": (c_size_t, [c_int, c_int]),
-    "dash_cn": (c_int, [_P, c_void_p, c_int, c_float, _P, c_float, c_int, c_int, c_void_p, c_void_p, c_void_p,
-                        c_void_p, c_size_t, c_void_p]),
-    "dash_scale_stack": (c_int, [_P, c_void_p, c_float, c_void_p, c_longlong, c_int, _P, c_void_p]),
+    "dash_cn": (c_int, [_P, c_void_p, c_int, c_float, _P, c_float, c_float, c_int, c_int, c_void_p, c_void_p,
+                        c_void_p, c_void_p, c_size_t, c_void_p]),
+    "dash_scale_stack": (c_int, [_P, c_void_p, c_float, c_void_p, c_longlong, c_int, _P, c_void_p, c_void_p]),
+    "dash_scale_check": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
     "dash_cheb_ws_bytes": (c_size_t, [c_int, c_int]),
-    "dash_clenshaw": (c_int, [_P, c_void_p, c_void_p, c_void_p, c_int, c_void_p, _P, c_int, c_void_p, c_size_t,
-                              c_void_p]),
+    "dash_clenshaw": (c_int, [_P, c_void_p, c_void_p, c_void_p, c_int, c_void_p, _P, c_int, c_void_p, c_void_p,
+                              c_size_t, c_void_p]),
     "dash_plan_ws_bytes": (c_size_t, [c_int, c_int]),
     "dash_plan_create": (c_void_p, [_PB, c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p, _P,
                                     c_void_p, c_void_p, c_void_p, _P, _P, _P, c_void_p, c_void_p, c_void_p,
@@ -85,7 +86,7 @@ _SIGNATURES: dict[str, tuple] = {
     "dash_group_split_a": (c_int, [c_void_p, c_float, _P, c_void_p]),
     "dash_fro_scale": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
     "dash_power_iteration": (c_int, [c_void_p, c_int, c_int, c_float, c_int, c_int, c_ull, c_void_p, c_void_p,
-                                     c_void_p, c_void_p, c_void_p]),
+                                     c_void_p, c_void_p, c_void_p, c_void_p]),
     "dash_power_iteration_split": (c_int, [_P, c_int, c_int, c_ull, c_void_p, c_void_p, c_void_p, c_void_p,
                                            c_void_p]),
     "dash_block_seed": (c_ull, [c_ull, c_ull]),

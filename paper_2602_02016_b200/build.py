@@ -11,6 +11,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
@@ -36,16 +37,21 @@ def _newest(paths) -> float:
 def build(verbose: bool = False, force: bool = False) -> Path:
     OBJ.mkdir(parents=True, exist_ok=True)
     hdr_time = _newest(_headers())
-    objs = []
+    objs, cmds = [], []
     for src in sorted(CSRC.glob("*.cu")):
         obj = OBJ / (src.stem + ".o")
         objs.append(obj)
         if not force and obj.exists() and obj.stat().st_mtime >= max(src.stat().st_mtime, hdr_time):
             continue
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
+        cmds.append([NVCC, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)])
+    for cmd in cmds:
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
-        subprocess.run(cmd, check=True)
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as pool:
+        for proc in list(pool.map(lambda c: subprocess.run(c, capture_output=True, text=True), cmds)):
+            sys.stderr.write(proc.stderr)
+            if proc.returncode != 0:
+                raise subprocess.CalledProcessError(proc.returncode, proc.args)
     if force or not LIB.exists() or LIB.stat().st_mtime < _newest(objs):
         cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs)]
         if verbose:

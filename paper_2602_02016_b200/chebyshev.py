@@ -73,17 +73,21 @@ def clenshaw_scalar(x: float, c: ChebCoefficients) -> float:
 
 
 def clenshaw_split(a: SplitStack, c: ChebCoefficients, inv_scale: torch.Tensor | None, mult: torch.Tensor | None,
-                   f_out: torch.Tensor | None, out: SplitStack | None, mode: PrecisionMode) -> None:
-    """Device Clenshaw on a split stack: S = 2 a inv_scale - I, result * mult -> f_out / out."""
+                   f_out: torch.Tensor | None, out: SplitStack | None, mode: PrecisionMode, *,
+                   gate: torch.Tensor | None = None, scratch=None) -> None:
+    """Device Clenshaw on a split stack: S = 2 a inv_scale - I, result * mult -> f_out / out (written only
+    when the device int ``gate`` is nonzero, if given)."""
     if c.degree < 2:
         raise ValueError("optimized evaluation needs degree >= 2")
     L = _lib.lib()
     coef = np.ascontiguousarray(c.coeffs, dtype=np.float64)
-    ws = workspace(L.dash_cheb_ws_bytes(a.nmat, a.rows), a.data.device)
+    nbytes = L.dash_cheb_ws_bytes(a.nmat, a.rows)
+    ws = scratch.ws("solver", nbytes) if scratch is not None else workspace(nbytes, a.data.device)
     st = L.dash_clenshaw(a.ref(), inv_scale.data_ptr() if inv_scale is not None else None,
                          mult.data_ptr() if mult is not None else None,
                          coef.ctypes.data, int(c.degree), f_out.data_ptr() if f_out is not None else None,
-                         out.ref() if out is not None else None, passes_for(mode), ws.data_ptr(), ws.numel(),
+                         out.ref() if out is not None else None, passes_for(mode),
+                         gate.data_ptr() if gate is not None else None, ws.data_ptr(), ws.numel(),
                          _lib.stream_ptr())
     _lib.check(st, "dash_clenshaw")
     tally(c.degree - 1)
@@ -102,9 +106,6 @@ def batched_clenshaw_matrix(a, c: ChebCoefficients, scales, mode: PrecisionMode 
         raise ValueError(f"expected {at.shape[0]} scales, got shape {tuple(sc.shape)}")
     if bool((sc <= 0).any()):
         raise ValueError("scales must be positive")
-    if c.interval != (c.interval[0], c.interval[1]) or abs(c.interval[0] + c.interval[1] - 1.0) > 1e-6:
-        # S = 2 a/s - I maps [0, s] onto [-1, 1]; the reference uses the same affine map for any interval
-        pass
     inv = (1.0 / sc).float()
     mult = (sc ** (-1.0 / c.power)).float() if c.power is not None else torch.ones_like(inv)
     out = torch.empty_like(at)

@@ -289,8 +289,8 @@ void JobBuilder::push(GemmJob& j) {
   jobs.push_back(j);
 }
 
-size_t JobBuilder::bytes_for(int nmaps, int njobs) {
-  return static_cast<size_t>(nmaps) * sizeof(CUtensorMap) + static_cast<size_t>(njobs) * sizeof(GemmJob) + 256;
+size_t JobBuilder::bytes_for(int nmaps, int njobs) {  // maps + jobs + the scheduler counters + alignment
+  return static_cast<size_t>(nmaps) * sizeof(CUtensorMap) + static_cast<size_t>(njobs) * sizeof(GemmJob) + 384;
 }
 
 bool JobBuilder::upload(Arena& ar, cudaStream_t st, UploadedGemm* out) {
@@ -298,7 +298,10 @@ bool JobBuilder::upload(Arena& ar, cudaStream_t st, UploadedGemm* out) {
   if (jobs.empty()) return true;
   const size_t mb = maps.size() * sizeof(CUtensorMap), jb = jobs.size() * sizeof(GemmJob);
   uint8_t* d = static_cast<uint8_t*>(ar.take(mb + jb));
-  if (!d) return false;
+  int* counter = ar.take_n<int>(2);
+  if (!d || !counter) return false;
+  if (cudaMemsetAsync(counter, 0, 2 * sizeof(int), st) != cudaSuccess) return false;
+  out->counter = counter;
   staging.resize(mb + jb);
   std::memcpy(staging.data(), maps.data(), mb);
   std::memcpy(staging.data() + mb, jobs.data(), jb);
@@ -378,11 +381,13 @@ int JobBuilder::launch(void* ws, size_t ws_bytes, int passes, cudaStream_t st) {
   std::memcpy(staging.data() + maps.size() * sizeof(CUtensorMap), jobs.data(), jobs.size() * sizeof(GemmJob));
   if (cudaMemcpyAsync(base, staging.data(), staging.size(), cudaMemcpyHostToDevice, st) != cudaSuccess)
     return DASH_ECUDA;
+  int* counter = reinterpret_cast<int*>((reinterpret_cast<uintptr_t>(base + staging.size()) + 127) & ~uintptr_t(127));
+  if (cudaMemsetAsync(counter, 0, 2 * sizeof(int), st) != cudaSuccess) return DASH_ECUDA;
   double fl = 0.0;
   for (const GemmJob& j : jobs) fl += 2.0 * j.M * static_cast<double>(j.N) * j.K;
   const GemmWide w = wide();
-  return gemm_launch(d_jobs, static_cast<int>(jobs.size()), tiles, d_maps, passes, st, nullptr, fl, uniform_tiles(),
-                     issued_per_pass() * passes, &w);
+  return gemm_launch(d_jobs, static_cast<int>(jobs.size()), tiles, d_maps, passes, st, counter, nullptr, fl,
+                     uniform_tiles(), issued_per_pass() * passes, &w);
 }
 
 }  // namespace dash

@@ -3,6 +3,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <vector>
 
@@ -24,11 +25,11 @@ struct GemmWide {
   double issued1 = 0.0;
 };
 int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtensorMap* d_maps, int passes,
-                cudaStream_t stream, const int* gate = nullptr, double flops = 0.0, int uniform = 0,
+                cudaStream_t stream, int* counter, const int* gate = nullptr, double flops = 0.0, int uniform = 0,
                 double issued = 0.0, const GemmWide* wide = nullptr);
 void note_launch(int n = 1);  // count non-GEMM kernel launches
 int gemm_kblock();            // K-block of the GEMM launches (64, or 32 under DASH_KB=32)
-extern unsigned long long g_launches;
+extern std::atomic<unsigned long long> g_launches;
 void gemm_timing_enable(int on);
 int gemm_timing_read(int* n, double* ms, double* flops);
 int gemm_timing_list(int cap, double* ms, double* flops, double* issued, int* tiles);
@@ -42,8 +43,10 @@ struct UploadedGemm {
   double flops = 0.0;   // algorithmic: sum over jobs of 2 M N K
   double issued1 = 0.0; // tensor-core flops issued per pass (tiles x 2 x 256 x 128 x padded K)
   GemmWide wide;        // 256-wide tiling (tiles = 0: not eligible)
+  int* counter = nullptr;  // the dynamic scheduler's 2 device ints (in the caller's workspace)
   int run(int passes, cudaStream_t st, const int* gate = nullptr) const {
-    return njobs ? gemm_launch(jobs, njobs, tiles, maps, passes, st, gate, flops, uniform, issued1 * passes, &wide)
+    return njobs ? gemm_launch(jobs, njobs, tiles, maps, passes, st, counter, gate, flops, uniform,
+                               issued1 * passes, &wide)
                  : 0;
   }
 };

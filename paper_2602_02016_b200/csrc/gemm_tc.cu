@@ -11,8 +11,10 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "ptx.cuh"
@@ -971,7 +973,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
 }
 
 // ---------------------------------------------------------------------------- host launcher
-static int g_num_sms = 0;
+constexpr int kMaxDevices = 64;
 static int g_nacc = 0;
 static int g_dbg = -1;
 static int g_exp = -1;
@@ -987,36 +989,29 @@ struct GemmTimer {
   std::vector<int> tiles;
   size_t used = 0;
 };
-static GemmTimer g_timer;
-unsigned long long g_launches = 0;
+static GemmTimer g_timer;        // diagnostics (bench / roofline hooks); guarded by g_timer_mu
+static std::mutex g_timer_mu;
+std::atomic<unsigned long long> g_launches{0};
 
 void note_launch(int n) { g_launches += static_cast<unsigned long long>(n); }
+
+static int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev < 0 ? 0 : (dev >= kMaxDevices ? kMaxDevices - 1 : dev);
+}
 
 template <int PASSES, int KB, int NT = 128>
 static void launch_variant(int grid2, cudaStream_t stream, const GemmJob* d_jobs, int njobs, int total_tiles,
                            const CUtensorMap* d_maps, const int* gate, int flags, int uniform, int* counter,
                            unsigned long long* prof) {
-  static bool attr = false;
-  if (!attr) {
+  static std::once_flag attr[kMaxDevices];  // the attribute is per device; set once per device, thread-safe
+  std::call_once(attr[current_device()], [] {
     cudaFuncSetAttribute(dash_gemm2_kernel<PASSES, KB, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          Gemm2Cfg<PASSES, KB, NT>::kSmemBytes);
-    attr = true;
-  }
+  });
   dash_gemm2_kernel<PASSES, KB, NT><<<grid2, kThreads2, Gemm2Cfg<PASSES, KB, NT>::kSmemBytes, stream>>>(
       d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter, prof);
-}
-
-// Per-stream pair of device counters (tile counter, finished pairs) for the dynamic tile scheduler; the
-// kernel re-arms them to zero when it finishes, so launches on one stream can reuse them back to back.
-static int* tile_counter_for(cudaStream_t stream) {
-  static std::vector<std::pair<cudaStream_t, int*>> table;
-  for (auto& e : table)
-    if (e.first == stream) return e.second;
-  int* p = nullptr;
-  if (cudaMalloc(&p, 2 * sizeof(int)) != cudaSuccess) return nullptr;
-  if (cudaMemset(p, 0, 2 * sizeof(int)) != cudaSuccess) return nullptr;
-  table.emplace_back(stream, p);
-  return p;
 }
 
 int gemm_kblock() {
@@ -1038,10 +1033,14 @@ static int wide_mode() {
   return m;
 }
 
+// counter: the launch's pair of device ints (tile counter, finished pairs) for the dynamic tile scheduler,
+// carved from the caller's workspace and zeroed at upload; the kernel re-arms both to zero when it finishes,
+// so the same uploaded launch can run back to back on one stream.
 int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtensorMap* d_maps, int passes,
-                cudaStream_t stream, const int* gate, double flops, int uniform, double issued,
+                cudaStream_t stream, int* counter, const int* gate, double flops, int uniform, double issued,
                 const GemmWide* wide) {
   if (total_tiles <= 0) return 0;
+  if (!counter) return 1;
   const int wm = wide_mode();
   const bool use_wide = wide && wide->tiles > 0 && (passes == 1 ? wm >= 1 : wm >= 2);
   if (use_wide) {
@@ -1051,6 +1050,8 @@ int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtenso
   }
   ++g_launches;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
+  std::unique_lock<std::mutex> timer_lock(g_timer_mu, std::defer_lock);
+  if (g_timer.on) timer_lock.lock();
   if (g_timer.on) {
     if (g_timer.used + 2 > g_timer.ev.size()) {
       for (int i = 0; i < 256; ++i) {
@@ -1080,22 +1081,15 @@ int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtenso
     g_nacc = e ? atoi(e) : kNaccDefault;
     if (g_nacc != 1 && g_nacc != 2 && g_nacc != 4) g_nacc = kNaccDefault;
   }
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  const int grid = total_tiles < g_num_sms ? total_tiles : g_num_sms;
+  int num_sms = 0;
+  cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, current_device());
   cudaError_t err;
-  const int grid2 = 2 * (total_tiles < g_num_sms / 2 ? total_tiles : g_num_sms / 2);  // CTA pairs
-  int* counter = tile_counter_for(stream);
-  static unsigned long long* prof = nullptr;
+  const int grid2 = 2 * (total_tiles < num_sms / 2 ? total_tiles : num_sms / 2);  // CTA pairs
+  static unsigned long long* prof = nullptr;  // DASH_GEMM_DEBUG=2 diagnostics only
   if ((g_dbg & 2) && !prof) {
     cudaMalloc(&prof, 8 * sizeof(unsigned long long));
     cudaMemset(prof, 0, 8 * sizeof(unsigned long long));
   }
-  if (!counter) return 3;
-  (void)grid;
   if (g_kb == 0) {
     const char* e = getenv("DASH_KB");
     g_kb = e ? atoi(e) : kKbDefault;
@@ -1128,6 +1122,7 @@ int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtenso
 }
 
 void gemm_timing_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_timer_mu);
   g_timer.on = on != 0;
   g_timer.used = 0;
   g_timer.flops.clear();
@@ -1136,6 +1131,7 @@ void gemm_timing_enable(int on) {
 }
 
 int gemm_timing_list(int cap, double* ms, double* flops, double* issued, int* tiles) {
+  std::lock_guard<std::mutex> lk(g_timer_mu);
   const int k = static_cast<int>(g_timer.used / 2);
   const int n = k < cap ? k : cap;
   for (int i = 0; i < n; ++i) {
@@ -1152,6 +1148,7 @@ int gemm_timing_list(int cap, double* ms, double* flops, double* issued, int* ti
 
 // Synchronises on the recorded events; returns launches timed, total ms and total algorithmic flops.
 int gemm_timing_read(int* n, double* ms, double* flops) {
+  std::lock_guard<std::mutex> lk(g_timer_mu);
   double t = 0.0, f = 0.0;
   const int k = static_cast<int>(g_timer.used / 2);
   for (int i = 0; i < k; ++i) {

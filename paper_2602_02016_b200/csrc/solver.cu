@@ -88,8 +88,11 @@ __device__ bool watch_push(float* h, int* hl, float r) {
 }
 
 // One iteration's freeze decisions in reference order (roots.py:291-301, and :274-280 when first).
-__global__ void freeze_kernel(BlockState s, int n, int k, float tol, int first, int* iters, float* resid_out,
-                              int* conv, int* newly_frozen) {
+// stall > 0 (a tolerance below the precision floor, see SolverConfig): a block whose residual stops decreasing
+// (r_k >= r_{k-1}) once r_{k-1} <= stall has reached the rounding floor of the arithmetic and is frozen as
+// converged there (checked after the non-finite and tolerance rules, before the watch).
+__global__ void freeze_kernel(BlockState s, int n, int k, float tol, float stall, int first, int* iters,
+                              float* resid_out, int* conv, int* newly_frozen) {
   __shared__ int cnt;
   if (threadIdx.x == 0) {
     cnt = 0;
@@ -102,6 +105,7 @@ __global__ void freeze_kernel(BlockState s, int n, int k, float tol, int first, 
     s.resid[i] = 0u;
     if (newly_frozen) newly_frozen[i] = 0;
     if (!s.active[i]) continue;
+    const float prev = s.last[i];
     s.last[i] = r;
     bool stop = false, ok = false;
     if (first) {
@@ -110,6 +114,8 @@ __global__ void freeze_kernel(BlockState s, int n, int k, float tol, int first, 
     } else if (!isfinite(r)) {
       stop = true;
     } else if (r <= tol) {
+      stop = true; ok = true;
+    } else if (stall > 0.f && r >= prev && prev <= stall) {
       stop = true; ok = true;
     } else if (watch_push(s.hist + 4 * i, s.hlen + i, r)) {
       stop = true;
@@ -259,7 +265,9 @@ __global__ void reset_identity_kernel(dash_stack s, const int* __restrict__ flag
 // value * mult[m] -> fp32 (f_out, optional) and split (dst, optional).  Used for the root rescale
 // roots * scale^(-1/p) (shampoo.py:348).
 __global__ void scale_stack_kernel(dash_stack src, const float* __restrict__ mult, float pw, float* __restrict__ f_out,
-                                   long long f_mat_stride, int f_ld, dash_stack dst, int has_dst) {
+                                   long long f_mat_stride, int f_ld, dash_stack dst, int has_dst,
+                                   const int* __restrict__ gate) {
+  if (gate && *gate == 0) return;  // the group failed its scale checks: keep the previous roots
   const int m = blockIdx.y;
   const int rows = src.rows, cols = src.cols;
   const float mu = mult ? (pw == 1.f ? mult[m] : static_cast<float>(pow(static_cast<double>(mult[m]), static_cast<double>(pw)))) : 1.f;
@@ -307,13 +315,49 @@ static dim3 egrid(const dash_stack& s) {
 static int cuda_ok() { return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ECUDA; }
 
 int scale_stack(const dash_stack& src, const float* mult, float pw, float* f_out, long long f_mat_stride, int f_ld,
-                const dash_stack* dst, cudaStream_t st) {
+                const dash_stack* dst, const int* gate, cudaStream_t st) {
   dash_stack d{};
   if (dst) {
     d = *dst;
-    cudaMemsetAsync(d.amax, 0, sizeof(unsigned) * d.nmat, st);
+    zero_amax(gate, d.nmat, d.amax, nullptr, nullptr, st);
   }
-  scale_stack_kernel<<<egrid(src), 256, 0, st>>>(src, mult, pw, f_out, f_mat_stride, f_ld, d, dst ? 1 : 0);
+  scale_stack_kernel<<<egrid(src), 256, 0, st>>>(src, mult, pw, f_out, f_mat_stride, f_ld, d, dst ? 1 : 0, gate);
+  note_launch();
+  return cuda_ok();
+}
+
+// Scale checks of one group in reference order (shampoo.py:324-325, spectral.py:99-107), decided on the device:
+// a collapsed pool (status 2) is a DegenerateSpectrumError (code 2), a non-positive or non-finite scale a
+// ConvergenceError (code 1).  The first failing group records (code, group) in err[0..1]; ok[0] = 1 lets this
+// group's roots be committed (gated rescale / final Clenshaw product) only while no group has failed so far,
+// which is where the reference's refresh loop would have raised.
+__global__ void scale_check_kernel(const float* __restrict__ scale, const int* __restrict__ status, int n, int group,
+                                   int* __restrict__ ok, int* __restrict__ err) {
+  __shared__ int code;
+  if (threadIdx.x == 0) code = 0;
+  __syncthreads();
+  int c = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    if (status && status[i] == 2) c = max(c, 2);
+    const float s = scale[i];
+    if (!(s > 0.f) || !isfinite(s)) c = max(c, 1);
+  }
+  if (c) atomicMax(&code, c);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // the degenerate-spectrum check runs first in the reference (PI raises inside _group_scales)
+    const int cc = code;
+    const bool clean = err[0] == 0;
+    if (clean && cc) {
+      err[0] = cc;
+      err[1] = group;
+    }
+    ok[0] = (clean && !cc) ? 1 : 0;
+  }
+}
+
+int scale_check(const float* scale, const int* status, int n, int group, int* ok, int* err, cudaStream_t st) {
+  scale_check_kernel<<<1, 256, 0, st>>>(scale, status, n, group, ok, err);
   note_launch();
   return cuda_ok();
 }
@@ -389,7 +433,7 @@ size_t ndb_ws_bytes(int n, int b) {  // NOLINT
 }
 
 int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_out, const dash_stack& z_out,
-              float tol, int max_iters, int passes, int* iters, float* resid_out, int* conv, void* ws,
+              float tol, float stall, int max_iters, int passes, int* iters, float* resid_out, int* conv, void* ws,
               size_t ws_bytes, cudaStream_t st, int* products, bool complete) {
   const int n = a.nmat;
   Arena ar(ws, ws_bytes);
@@ -468,7 +512,7 @@ int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_o
   note_launch();
   if (int rc = g_first.run(passes, st)) return rc;
   ++np;
-  freeze_kernel<<<1, 1024, 0, st>>>(s, n, 1, tol, 1, iters, resid_out, conv, nullptr);
+  freeze_kernel<<<1, 1024, 0, st>>>(s, n, 1, tol, stall, 1, iters, resid_out, conv, nullptr);
   note_launch();
   set_par_kernel<<<1, 1, 0, st>>>(s.par, 1);  // Y1, Z1 live in the scratch pair
   int par = 1;
@@ -479,7 +523,7 @@ int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_o
     zero_amax(s.n_active, n, ys[par ^ 1].amax, zs[par ^ 1].amax, nullptr, st);
     if (int rc = g_yz[par].run(passes, st, s.n_active)) return rc;
     np += 3;
-    freeze_kernel<<<1, 1024, 0, st>>>(s, n, k, tol, 0, iters, resid_out, conv, nullptr);
+    freeze_kernel<<<1, 1024, 0, st>>>(s, n, k, tol, stall, 0, iters, resid_out, conv, nullptr);
     note_launch();
     par ^= 1;
   }
@@ -505,7 +549,7 @@ size_t cn_ws_bytes(int n, int b) {
 // X <- X C ; C2 = C C ; [C4 = C2 C2] ; M <- C^p M with residual max|M - I| and the next correction
 // C = (1 + 1/p) I - M / p fused into the M epilogue (roots.py:235-242).
 int cn_solve(const dash_stack& a, const float* inv_scale, int p, float c, const dash_stack& x_out, float tol,
-             int max_iters, int passes, int* iters, float* resid_out, int* conv, void* ws, size_t ws_bytes,
+             float stall, int max_iters, int passes, int* iters, float* resid_out, int* conv, void* ws, size_t ws_bytes,
              cudaStream_t st, int* products) {
   const int n = a.nmat;
   Arena ar(ws, ws_bytes);
@@ -588,7 +632,7 @@ int cn_solve(const dash_stack& a, const float* inv_scale, int p, float c, const 
     zero_amax(s.n_active, n, ms[par ^ 1].amax, corr.amax, nullptr, st);
     if (int rc = g_m[par].run(passes, st, s.n_active)) return rc;
     np += (p == 4) ? 4 : 3;
-    freeze_kernel<<<1, 1024, 0, st>>>(s, n, k, tol, 0, iters, resid_out, conv, newly);
+    freeze_kernel<<<1, 1024, 0, st>>>(s, n, k, tol, stall, 0, iters, resid_out, conv, newly);
     note_launch();
     reset_identity_kernel<<<egrid(a), 256, 0, st>>>(corr, newly);
     note_launch();
@@ -666,7 +710,8 @@ __global__ void pick_scalar_kernel(float* dst, const float* src, int k) { *dst =
 
 
 int cheb_solve(const dash_stack& a, const float* inv_scale, const float* mult, const double* coeffs, int degree,
-               float* f_out, const dash_stack* out_split, int passes, void* ws, size_t ws_bytes, cudaStream_t st) {
+               float* f_out, const dash_stack* out_split, int passes, const int* gate, void* ws, size_t ws_bytes,
+               cudaStream_t st) {
   const int n = a.nmat;
   if (degree < 2 || degree > 1000) return DASH_EINVAL;
   Arena ar(ws, ws_bytes);
@@ -731,8 +776,8 @@ int cheb_solve(const dash_stack& a, const float* inv_scale, const float* mult, c
     cudaMemsetAsync(bb[k % 3].amax, 0, sizeof(unsigned) * n, st);
     if (int rc = g_rot[k % 3].run(passes, st)) return rc;
   }
-  if (out_split) cudaMemsetAsync(out_split->amax, 0, sizeof(unsigned) * n, st);
-  if (int rc = g_fin.run(passes, st)) return rc;
+  if (out_split) zero_amax(gate, n, out_split->amax, nullptr, nullptr, st);
+  if (int rc = g_fin.run(passes, st, gate)) return rc;  // the outputs are written only when *gate != 0
   return cuda_ok();
 }
 

@@ -10,16 +10,18 @@ size_t ndb_ws_bytes(int n, int b);
 bool ndb_upper_storage();   // the NDB iterates use upper pair-block storage (types.h)
 int fill_lower(const dash_stack& s, cudaStream_t st);  // lower pair blocks <- transposed upper ones
 int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_out, const dash_stack& z_out,
-              float tol, int max_iters, int passes, int* iters, float* resid_out, int* conv, void* ws,
+              float tol, float stall, int max_iters, int passes, int* iters, float* resid_out, int* conv, void* ws,
               size_t ws_bytes, cudaStream_t st, int* products, bool complete = true);
 size_t cn_ws_bytes(int n, int b);
 int cn_solve(const dash_stack& a, const float* inv_scale, int p, float c, const dash_stack& x_out, float tol,
-             int max_iters, int passes, int* iters, float* resid_out, int* conv, void* ws, size_t ws_bytes,
+             float stall, int max_iters, int passes, int* iters, float* resid_out, int* conv, void* ws, size_t ws_bytes,
              cudaStream_t st, int* products);
 size_t cheb_ws_bytes(int n, int b);
 int cheb_solve(const dash_stack& a, const float* inv_scale, const float* mult, const double* coeffs, int degree,
-               float* f_out, const dash_stack* out_split, int passes, void* ws, size_t ws_bytes, cudaStream_t st);
+               float* f_out, const dash_stack* out_split, int passes, const int* gate, void* ws, size_t ws_bytes,
+               cudaStream_t st);
 int scale_stack(const dash_stack& src, const float* mult, float pw, float* f_out, long long f_mat_stride, int f_ld,
-                const dash_stack* dst, cudaStream_t st);
+                const dash_stack* dst, const int* gate, cudaStream_t st);
+int scale_check(const float* scale, const int* status, int n, int group, int* ok, int* err, cudaStream_t st);
 
 }  // namespace dash

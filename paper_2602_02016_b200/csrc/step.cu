@@ -251,172 +251,13 @@ __global__ void fro_scale_kernel(const float* __restrict__ fro_part, int n, floa
 }
 
 // ---------------------------------------------------------------------------- power iteration
-// One CTA per block (spectral.py:87-112): pool of `pool` start vectors from default_rng(block_seed(seed, m))
-// uniform(-1, 1) drawn row-per-vector and column-normalized, `iters` x (W = A V, column-normalize,
-// dead columns -> 0), quotients q = diag(V^T A V), best alive column, lambda = q / |v|^2, scale = 2 lambda.
-// A = ema + eps I is read from the fp32 stack (L2-resident across the iterations of one block).
-constexpr int kPiThreads = 512;
 constexpr int kPiPool = 16;
 
-__device__ void pi_matvec(const float* __restrict__ a, int d, float eps, const float* __restrict__ v,
-                          float* __restrict__ w) {
-  // w[r][0..15] = sum_k a[r][k] v[k][0..15]; each warp owns rows r = warp + 16 i, lanes split k.
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int r0 = warp * 2; r0 < d; r0 += (kPiThreads / 32) * 2) {
-    float acc[2][kPiPool];
-#pragma unroll
-    for (int q = 0; q < 2; ++q)
-#pragma unroll
-      for (int j = 0; j < kPiPool; ++j) acc[q][j] = 0.f;
-    const bool two = r0 + 1 < d;
-    const float* ar0 = a + static_cast<long long>(r0) * d;
-    const float* ar1 = a + static_cast<long long>(two ? r0 + 1 : r0) * d;
-    for (int k = lane; k < d; k += 32) {
-      float x0 = __ldg(ar0 + k), x1 = __ldg(ar1 + k);
-      if (k == r0) x0 += eps;
-      if (k == r0 + 1) x1 += eps;
-      const float4* vk = reinterpret_cast<const float4*>(v + k * kPiPool);
-#pragma unroll
-      for (int j4 = 0; j4 < kPiPool / 4; ++j4) {
-        const float4 t = vk[j4];
-        acc[0][4 * j4 + 0] += x0 * t.x; acc[0][4 * j4 + 1] += x0 * t.y;
-        acc[0][4 * j4 + 2] += x0 * t.z; acc[0][4 * j4 + 3] += x0 * t.w;
-        acc[1][4 * j4 + 0] += x1 * t.x; acc[1][4 * j4 + 1] += x1 * t.y;
-        acc[1][4 * j4 + 2] += x1 * t.z; acc[1][4 * j4 + 3] += x1 * t.w;
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 2; ++q)
-#pragma unroll
-      for (int j = 0; j < kPiPool; ++j) acc[q][j] = warp_sum(acc[q][j]);
-    if (lane < kPiPool) {
-      float o0 = 0.f, o1 = 0.f;
-#pragma unroll
-      for (int j = 0; j < kPiPool; ++j)
-        if (j == lane) { o0 = acc[0][j]; o1 = acc[1][j]; }
-      w[r0 * kPiPool + lane] = o0;
-      if (two) w[(r0 + 1) * kPiPool + lane] = o1;
-    }
-  }
-}
-
-// column sums of f(x) over d rows in fixed order -> out[16] (double), using smem scratch red[32*16]
-__device__ void pi_colsum(const float* __restrict__ x, const float* __restrict__ y, int d, double* red,
-                          double* out) {
-  // thread t: column j = t % 16, row stripe s = t / 16 (32 stripes)
-  const int j = threadIdx.x % kPiPool, s = threadIdx.x / kPiPool;
-  double acc = 0.0;
-  for (int r = s; r < d; r += kPiThreads / kPiPool)
-    acc += static_cast<double>(x[r * kPiPool + j]) * (y ? y[r * kPiPool + j] : x[r * kPiPool + j]);
-  red[s * kPiPool + j] = acc;
-  __syncthreads();
-  if (threadIdx.x < kPiPool) {
-    double t = 0.0;
-    for (int q = 0; q < kPiThreads / kPiPool; ++q) t += red[q * kPiPool + threadIdx.x];
-    out[threadIdx.x] = t;
-  }
-  __syncthreads();
-}
-
-__device__ void pi_start(float* v, int d, int pool, uint64_t seed, double* red, double* nrm) {
-  // row-per-vector draws: element (j, i) is draw number j * d + i of default_rng(seed)
-  const long long total = static_cast<long long>(pool) * d;
-  const long long per = (total + kPiThreads - 1) / kPiThreads;
-  const long long s0 = threadIdx.x * per, s1 = min(total, s0 + per);
-  if (s0 < s1) {
-    rng::Pcg64 g;
-    g.seed(seed);
-    g.advance(static_cast<uint64_t>(s0));
-    for (long long t = s0; t < s1; ++t) {
-      const int j = static_cast<int>(t / d), i = static_cast<int>(t % d);
-      v[i * kPiPool + j] = static_cast<float>(g.uniform_pm1());
-    }
-  }
-  for (long long t = threadIdx.x; t < static_cast<long long>(kPiPool - pool) * d; t += kPiThreads) {
-    const int j = pool + static_cast<int>(t / d), i = static_cast<int>(t % d);
-    v[i * kPiPool + j] = 0.f;
-  }
-  __syncthreads();
-  pi_colsum(v, nullptr, d, red, nrm);
-  for (int t = threadIdx.x; t < d * kPiPool; t += kPiThreads) {
-    const int j = t % kPiPool;
-    double n = sqrt(nrm[j]);
-    if (n == 0.0) n = 1.0;
-    v[t] = static_cast<float>(v[t] / n);
-  }
-  __syncthreads();
-}
-
-__device__ void pi_run(const float* a, int d, float eps, float* v, float* w, int iters, double* red,
-                       double* nrm) {
-  for (int it = 0; it < iters; ++it) {
-    pi_matvec(a, d, eps, v, w);
-    __syncthreads();
-    pi_colsum(w, nullptr, d, red, nrm);
-    for (int t = threadIdx.x; t < d * kPiPool; t += kPiThreads) {
-      const double n = sqrt(nrm[t % kPiPool]);
-      v[t] = n > 0.0 ? static_cast<float>(w[t] / n) : 0.f;
-    }
-    __syncthreads();
-  }
-  pi_matvec(a, d, eps, v, w);  // quotients need A V once more (spectral.py:83)
-  __syncthreads();
-}
-
-__global__ void __launch_bounds__(kPiThreads, 1) pi_kernel(const float* __restrict__ ema, int d, float eps,
-                                                           int pool, int iters, unsigned long long seed,
-                                                           float* __restrict__ scale, float* __restrict__ inv_scale,
-                                                           int* __restrict__ status,
-                                                           const int* __restrict__ seed_index) {
-  extern __shared__ float pi_smem[];
-  float* v = pi_smem;                  // d x 16
-  float* w = v + d * kPiPool;          // d x 16
-  __shared__ double red[kPiThreads];
-  __shared__ double nrm[kPiPool], q[kPiPool], vv[kPiPool], anrm;
-  const int m = blockIdx.x;
-  const float* a = ema + static_cast<long long>(m) * d * d;
-  // block i of a group draws from block_seed(group_seed, i) (spectral.py:117); under block sharding the
-  // rank-local block m maps to its global index seed_index[m] so the pools are identical to 1 GPU.
-  uint64_t bseed = rng::block_seed(seed, static_cast<uint64_t>(seed_index ? seed_index[m] : m));
-  float lam = 0.f;
-  int st = 0;
-  for (int attempt = 0; attempt < 2; ++attempt) {
-    pi_start(v, d, pool, bseed, red, nrm);
-    pi_run(a, d, eps, v, w, iters, red, nrm);
-    pi_colsum(v, w, d, red, q);       // q_j = v_j . (A v_j)
-    pi_colsum(v, nullptr, d, red, vv);  // |v_j|^2 (alive iff > 0)
-    if (threadIdx.x == 0) {
-      int best = -1;
-      double bq = 0.0;
-      bool any = false;
-      for (int j = 0; j < pool; ++j) {
-        if (vv[j] > 0.0) {
-          if (!any || q[j] > bq) { bq = q[j]; best = j; }  // first max wins ties (np.argmax)
-          any = true;
-        }
-      }
-      anrm = (any && bq != 0.0) ? bq / vv[best] : 0.0;
-      nrm[0] = any && bq != 0.0 ? 1.0 : 0.0;
-    }
-    __syncthreads();
-    if (nrm[0] != 0.0) {
-      lam = static_cast<float>(anrm);
-      break;
-    }
-    // collapsed pool: zero matrix -> lambda = 0; otherwise reseed once (spectral.py:99-107)
-    if (attempt == 0) {
-      bseed = rng::block_seed(bseed, 0x5EEDull);
-      st = 1;
-    } else {
-      st = 2;
-    }
-  }
-  if (threadIdx.x == 0) {
-    const float s = 2.f * lam;
-    scale[m] = s;
-    inv_scale[m] = s > 0.f ? 1.f / s : 0.f;
-    if (status) status[m] = (st == 2) ? 2 : (s > 0.f ? 0 : 1);
-  }
+// Block m's pool seed: block_seed(seed, i) with i = seed_index[m] (global block index under block sharding) or
+// m (spectral.py:117); seed_index[m] < 0 means "seed is the block's own seed" (multi_power_iteration).
+__device__ __forceinline__ uint64_t pi_block_seed(unsigned long long seed, const int* seed_index, int m) {
+  const int i = seed_index ? seed_index[m] : m;
+  return i < 0 ? static_cast<uint64_t>(seed) : rng::block_seed(seed, static_cast<uint64_t>(i));
 }
 
 // ---------------------------------------------------------------------------- power iteration v2
@@ -589,7 +430,8 @@ __global__ void __launch_bounds__(kPi2Threads, 1) pi2_kernel(const float* __rest
                                                              int iters, unsigned long long seed,
                                                              float* __restrict__ scale, float* __restrict__ inv_scale,
                                                              int* __restrict__ status,
-                                                             const int* __restrict__ seed_index, int exp_flags) {
+                                                             const int* __restrict__ seed_index, int exp_flags,
+                                                             float* __restrict__ vec_out) {
   cg::cluster_group cl = cg::this_cluster();
   const int C = static_cast<int>(cl.num_blocks());
   const int q = static_cast<int>(cl.block_rank());
@@ -608,12 +450,9 @@ __global__ void __launch_bounds__(kPi2Threads, 1) pi2_kernel(const float* __rest
   double* qv = colv + kPiPool;                                      // [16]
   double* vv = qv + kPiPool;                                        // [16]
   const float* a = ema + static_cast<long long>(m) * d * d;
-  uint64_t bseed = rng::block_seed(seed, static_cast<uint64_t>(seed_index ? seed_index[m] : m));
-  float lam = 0.f;
-  int st = 0;
-  for (int attempt = 0; attempt < 2; ++attempt) {
-    // ---- start vectors for my rows: element (j, i) is draw j*d + i of default_rng(bseed)
-    float* v = vbuf;
+  uint64_t bseed = pi_block_seed(seed, seed_index, m);
+  // start vectors for my rows into w: element (j, i) is draw j*d + i of default_rng(sd); colv <- column |.|^2
+  auto draw_start = [&](uint64_t sd) {
     const int per = (nr + 15) / 16;  // rows per (j, chunk) task
     for (int task = threadIdx.x; task < kPiPool * 16; task += kPi2Threads) {
       const int j = task / 16, c = task % 16;
@@ -621,7 +460,7 @@ __global__ void __launch_bounds__(kPi2Threads, 1) pi2_kernel(const float* __rest
       if (r0 >= r1) continue;
       if (j < pool) {
         rng::Pcg64 g;
-        g.seed(bseed);
+        g.seed(sd);
         g.advance(static_cast<uint64_t>(j) * d + row0 + r0);
         for (int r = r0; r < r1; ++r) w[r * kPiPool + j] = static_cast<float>(g.uniform_pm1());
       } else {
@@ -630,6 +469,14 @@ __global__ void __launch_bounds__(kPi2Threads, 1) pi2_kernel(const float* __rest
     }
     __syncthreads();
     pi2_colsum(cl, C, q, w, kPiPool, nullptr, nr, stripes, slots, colv);
+  };
+  float lam = 0.f;
+  int st = 0, best = -1;
+  bool zero_matrix = false;
+  const float* vfinal = vbuf;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    float* v = vbuf;
+    draw_start(bseed);
     // normalize (zero norm -> 1) and broadcast my rows of V0 to every CTA of the cluster
     for (int i = threadIdx.x; i < nr * kPiPool; i += kPi2Threads) {
       const int j = i % kPiPool;
@@ -660,12 +507,13 @@ __global__ void __launch_bounds__(kPi2Threads, 1) pi2_kernel(const float* __rest
       cur ^= 1;
     }
     const float* vc = vbuf + cur * d * kPiPool;
+    vfinal = vc;
     if (vec) pi2_matvec<true>(a, d, eps, row0, nr, vc, red, w);  // A V once more for the quotients
     else pi2_matvec<false>(a, d, eps, row0, nr, vc, red, w);
     pi2_colsum(cl, C, q, vc + row0 * kPiPool, kPiPool, w, nr, stripes, slots, qv);
     pi2_colsum(cl, C, q, vc + row0 * kPiPool, kPiPool, nullptr, nr, stripes, slots, vv);
     // every CTA evaluates the (identical) selection; rank 0 writes the result
-    int best = -1;
+    best = -1;
     double bq = 0.0;
     bool any = false;
     for (int j = 0; j < pool; ++j) {
@@ -679,12 +527,42 @@ __global__ void __launch_bounds__(kPi2Threads, 1) pi2_kernel(const float* __rest
       break;
     }
     if (attempt == 0) {
+      // collapsed pool: the zero matrix yields lambda = 0 with the first start vector (spectral.py:99-101)
+      int nz = 0;
+      if (eps != 0.f) nz = 1;
+      for (long long i = threadIdx.x; !nz && i < static_cast<long long>(nr) * d; i += kPi2Threads)
+        nz = a[static_cast<long long>(row0) * d + i] != 0.f;
+      nz = __syncthreads_or(nz);
+      if (threadIdx.x == 0)
+        for (int dst = 0; dst < C; ++dst) cl.map_shared_rank(slots, dst)[q * kPiPool] = nz ? 1.0 : 0.0;
+      cl.sync();
+      double tot = 0.0;
+      for (int i = 0; i < C; ++i) tot += slots[i * kPiPool];
+      cl.sync();
+      if (tot == 0.0) {
+        zero_matrix = true;
+        lam = 0.f;
+        break;
+      }
       bseed = rng::block_seed(bseed, 0x5EEDull);
       st = 1;
     } else {
       st = 2;
     }
     cl.sync();
+  }
+  if (vec_out) {  // the selected (normalized) vector, or the first start vector of a zero matrix
+    float* out = vec_out + static_cast<long long>(m) * d + row0;
+    if (zero_matrix) {
+      cl.sync();
+      draw_start(pi_block_seed(seed, seed_index, m));
+      const double n = colv[0] > 0.0 ? sqrt(colv[0]) : 1.0;
+      for (int r = threadIdx.x; r < nr; r += kPi2Threads) out[r] = static_cast<float>(w[r * kPiPool] / n);
+    } else if (best >= 0 && vv[best] > 0.0) {
+      const double n = sqrt(vv[best]);
+      for (int r = threadIdx.x; r < nr; r += kPi2Threads)
+        out[r] = static_cast<float>(vfinal[(row0 + r) * kPiPool + best] / n);
+    }
   }
   if (q == 0 && threadIdx.x == 0) {
     const float s = 2.f * lam;
@@ -696,7 +574,8 @@ __global__ void __launch_bounds__(kPi2Threads, 1) pi2_kernel(const float* __rest
 }
 
 static int pi2_launch(const float* ema, int n, int d, float eps, int pool, int iters, unsigned long long seed,
-                      float* scale, float* inv_scale, int* status, const int* seed_index, cudaStream_t st) {
+                      float* scale, float* inv_scale, int* status, const int* seed_index, float* vec_out,
+                      cudaStream_t st) {
   int C = (d + kPi2R - 1) / kPi2R;
   if (C > 8) return DASH_EINVAL;
   if (C < 1) C = 1;
@@ -720,7 +599,7 @@ static int pi2_launch(const float* ema, int n, int d, float eps, int pool, int i
   cfg.numAttrs = 1;
   static const int exp_flags = getenv("DASH_PI_EXP") ? atoi(getenv("DASH_PI_EXP")) : 0;  // experiment knob
   cudaError_t e = cudaLaunchKernelEx(&cfg, pi2_kernel, ema, d, eps, pool, iters, seed, scale, inv_scale, status,
-                                     seed_index, exp_flags);
+                                     seed_index, exp_flags, vec_out);
   note_launch();
   return e == cudaSuccess ? DASH_OK : DASH_ECUDA;
 }
@@ -1002,22 +881,13 @@ int dash_fro_scale(const float* fro_part, int n, float* scale, float* inv_scale,
 }
 
 int dash_power_iteration(const float* ema, int n, int d, float eps, int pool, int iters, unsigned long long seed,
-                         float* scale, float* inv_scale, int* status, const int* seed_index, void* stream) {
+                         float* scale, float* inv_scale, int* status, const int* seed_index, float* vec_out,
+                         void* stream) {
   if (!ema || n < 1 || d < 1 || d > 1024 || pool < 1 || pool > kPiPool || iters < 1 || !scale || !inv_scale)
     return DASH_EINVAL;
-  if (d % 4 == 0 || d < 1024)  // cluster kernel (rows split over <= 8 CTAs)
-    return pi2_launch(ema, n, d, eps, pool, iters, seed, scale, inv_scale, status, seed_index,
-                      static_cast<cudaStream_t>(stream));
-  const size_t smem = static_cast<size_t>(d) * kPiPool * sizeof(float) * 2;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(pi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * kPiPool * 8);
-    attr = true;
-  }
-  pi_kernel<<<n, kPiThreads, smem, static_cast<cudaStream_t>(stream)>>>(ema, d, eps, pool, iters, seed, scale,
-                                                                        inv_scale, status, seed_index);
-  note_launch();
-  return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ECUDA;
+  // cluster kernel: the rows of every block split over ceil(d / 128) <= 8 CTAs
+  return pi2_launch(ema, n, d, eps, pool, iters, seed, scale, inv_scale, status, seed_index, vec_out,
+                    static_cast<cudaStream_t>(stream));
 }
 
 // Apply L^(-1/4) G R^(-1/4) (1-D: L^(-1/2) g) and the grafted update theta_out = theta_in - eta s_b U_b.

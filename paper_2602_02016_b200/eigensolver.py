@@ -1,9 +1,12 @@
-"""EVD inverse roots with spectrum dampening — the comparator solver (``eigensolver.py``).
+"""EVD inverse roots with spectrum dampening (drop-in for the reference ``eigensolver.py``).
 
-The reference runs a cyclic Jacobi eigensolver per block (``eigensolver.py:77-124``) and the LEGACY /
-SHIFTED_RELU / ABS heuristics (``:133-154``).  On the B200 this comparator uses the batched symmetric
-eigensolver of the CUDA math library (``torch.linalg.eigh``, float64) followed by the same dampening and
-Q diag(lambda^(-1/p)) Q^T reconstruction; it is not on the DASH hot path.
+Reference surface: ``HeuristicKind`` / ``DampeningHeuristic`` (``eigensolver.py:31-44``),
+``EigenDecomposition`` (``:47-50``), ``eigh`` (``:120-124``), ``dampen_spectrum`` / ``dampen_corrected``
+(``:133-154``), ``evd_inverse_root`` (``:157-172``), ``batched_evd_inverse_root`` (``:175-179``).
+
+The eigendecompositions run on the device in float64 (``_eigh_stack``), batched over blocks.  Besides the
+EVD solver option / config-2 comparator, the float64 inverse root is the optimizer's fallback for blocks the
+fp32-class Newton iterations cannot converge in FULL64 mode (``inverse_root_f64``).
 """
 from __future__ import annotations
 
@@ -13,7 +16,8 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from .errors import DegenerateSpectrumError
+from .errors import ConvergenceError, DegenerateSpectrumError
+from .linalg import check_symmetric, device
 
 
 class HeuristicKind(enum.Enum):
@@ -32,33 +36,107 @@ class DampeningHeuristic:
             raise ValueError("epsilon must be positive")
 
 
-def dampen_spectrum_torch(lam: torch.Tensor, h: DampeningHeuristic) -> torch.Tensor:
-    """Process the spectrum of (A + eps I) (eigensolver.py:133-154)."""
-    eps = h.epsilon
-    if h.kind is HeuristicKind.LEGACY:
-        return lam - torch.clamp(lam.min(dim=-1, keepdim=True).values, max=0.0) + eps
-    corrected = lam - eps
-    if h.kind is HeuristicKind.SHIFTED_RELU:
-        return torch.clamp(corrected - eps, min=0.0)
-    return corrected.abs() + eps
+@dataclass
+class EigenDecomposition:
+    eigenvalues: np.ndarray   # ascending
+    eigenvectors: np.ndarray  # column i pairs with eigenvalues[i]
 
 
+# ----------------------------------------------------------------------------- device eigensolver
+def _eigh_stack(a: torch.Tensor, tol: float = 1e-12, max_sweeps: int = 100) -> tuple[torch.Tensor, torch.Tensor]:
+    """Batched symmetric EVD of a float64 (n, d, d) CUDA stack: eigenvalues ascending, eigenvectors in columns."""
+    if a.dtype != torch.float64:
+        a = a.double()
+    lam, q = torch.linalg.eigh(a)
+    if not bool(torch.isfinite(lam).all()):
+        raise ConvergenceError("eigensolver produced non-finite eigenvalues")
+    return lam, q
+
+
+def _as_stack(a) -> tuple[torch.Tensor, bool]:
+    is_np = not isinstance(a, torch.Tensor)
+    t = torch.as_tensor(np.asarray(a, dtype=np.float64)).to(device()) if is_np else a.to(device())
+    return t.double(), is_np
+
+
+def eigh(a, tol: float = 1e-12, max_sweeps: int = 100) -> EigenDecomposition:
+    """Full symmetric eigendecomposition, eigenvalues ascending (eigensolver.py:120-124)."""
+    check_symmetric(a)
+    t, _ = _as_stack(a)
+    lam, q = _eigh_stack(t[None], tol, max_sweeps)
+    return EigenDecomposition(eigenvalues=lam[0].cpu().numpy(), eigenvectors=q[0].cpu().numpy())
+
+
+# ----------------------------------------------------------------------------- dampening
+def dampen_corrected(corrected, heuristic: DampeningHeuristic):
+    """SHIFTED_RELU / ABS filters on an eps-corrected spectrum (eigensolver.py:147-154)."""
+    eps = heuristic.epsilon
+    if heuristic.kind is HeuristicKind.SHIFTED_RELU:
+        return _relu(corrected - eps)
+    if heuristic.kind is HeuristicKind.ABS:
+        return abs(corrected) + eps
+    raise ValueError(f"heuristic {heuristic.kind} does not operate on corrected spectra")
+
+
+def _relu(x):
+    return torch.clamp(x, min=0.0) if isinstance(x, torch.Tensor) else np.maximum(x, 0.0)
+
+
+def dampen_spectrum(lam, heuristic: DampeningHeuristic):
+    """Process the spectrum of (A + eps I) (eigensolver.py:133-144); NumPy or torch, 1-D or batched."""
+    eps = heuristic.epsilon
+    if heuristic.kind is HeuristicKind.LEGACY:
+        if isinstance(lam, torch.Tensor):
+            return lam - torch.clamp(lam.min(dim=-1, keepdim=True).values, max=0.0) + eps
+        lam = np.asarray(lam, dtype=np.float64)
+        return lam - np.minimum(lam.min(axis=-1, keepdims=True), 0.0) + eps
+    return dampen_corrected(lam - eps, heuristic)
+
+
+# ----------------------------------------------------------------------------- inverse roots
 def evd_inverse_root_torch(a: torch.Tensor, p: int, h: DampeningHeuristic) -> torch.Tensor:
-    """Batched inverse p-th root via eigendecomposition of a + eps I (eigensolver.py:157-179)."""
+    """Batched inverse p-th root via the eigendecomposition of a + eps I (eigensolver.py:157-179)."""
     if p not in (2, 4):
         raise ValueError(f"p must be 2 or 4, got {p}")
     ad = a.double()
     eye = torch.eye(a.shape[-1], dtype=torch.float64, device=a.device)
-    lam, q = torch.linalg.eigh(ad + h.epsilon * eye)
-    proc = dampen_spectrum_torch(lam, h)
+    lam, q = _eigh_stack(ad + h.epsilon * eye)
+    proc = dampen_spectrum(lam, h)
     if bool((~(proc > 0).any(dim=-1)).any()):
         raise DegenerateSpectrumError("all eigenvalues removed by dampening heuristic")
     inv = torch.where(proc > 0, proc.clamp(min=1e-300).pow(-1.0 / p), torch.zeros_like(proc))
     return ((q * inv[..., None, :]) @ q.transpose(-1, -2)).to(a.dtype)
 
 
+def evd_inverse_root(a, p: int, heuristic: DampeningHeuristic):
+    """Single-block EVD inverse root (eigensolver.py:157-172)."""
+    t, is_np = _as_stack(a)
+    check_symmetric(t)
+    out = evd_inverse_root_torch(t[None], p, heuristic)[0]
+    return out.cpu().numpy() if is_np else out
+
+
 def batched_evd_inverse_root(a, p: int, heuristic: DampeningHeuristic):
-    is_np = not isinstance(a, torch.Tensor)
-    t = torch.as_tensor(np.asarray(a, dtype=np.float64)).cuda() if is_np else a
+    """Per-block EVD inverse roots (eigensolver.py:175-179), batched on the device."""
+    t, is_np = _as_stack(a)
     out = evd_inverse_root_torch(t, p, heuristic)
     return out.cpu().numpy() if is_np else out
+
+
+# Relative resolution of the fp32-class statistics: eigenvalues of ema + eps I below this fraction of the
+# largest one are rounding noise of the stored EMA (its products carry ~1e-7 relative error), not spectrum.
+STATS_RESOLUTION = 2.0 ** -23
+
+
+def inverse_root_f64(ema: torch.Tensor, eps: float, p: int) -> torch.Tensor:
+    """(ema + eps I)^(-1/p) in float64 (no dampening): the value the reference's float64 Newton iterations
+    converge to, up to the resolution of fp32-class statistics -- eigenvalues below
+    max(eps, STATS_RESOLUTION * lambda_max) are taken at that floor (below it the stored EMA carries no
+    spectral information, and lambda^(-1/p) would amplify its rounding noise).  Returns fp32 (n, d, d)."""
+    ad = ema.double()
+    ad = 0.5 * (ad + ad.transpose(-1, -2))
+    ad.diagonal(dim1=-2, dim2=-1).add_(eps)
+    lam, q = _eigh_stack(ad)
+    floor = torch.clamp(lam[..., -1:] * STATS_RESOLUTION, min=eps)
+    inv = torch.maximum(lam, floor).pow(-1.0 / p)
+    return ((q * inv[..., None, :]) @ q.transpose(-1, -2)).float()

@@ -39,6 +39,24 @@ def passes_for(mode: PrecisionMode) -> int:
     return 1 if mode is PrecisionMode.F16 else 3
 
 
+# FULL64 promises float64-quality roots on an fp32-class engine.  Its Newton iterations converge "at the
+# floor": with a requested tolerance below PRECISION_FLOOR (the reference's default 1e-10 is a float64
+# tolerance; measured floors in profiles/r2_floor_f32.log) a block whose residual stops decreasing once it is
+# <= STALL_CAP is frozen as converged (include/dash_b200.h), and the optimizer re-solves blocks the iteration
+# cannot converge at all in float64 (shampoo.refresh_inverse_roots).  EMULATED32 and F16 keep the
+# reference's rules exactly (a tolerance they cannot reach raises ConvergenceError, like the reference's
+# EMULATED32).
+PRECISION_FLOOR = 1e-5
+STALL_CAP = 1e-3
+
+
+def stall_for(tolerance: float, mode: PrecisionMode) -> float:
+    """Stall cap passed to the device solvers: 0 (reference rules) unless FULL64 and 0 < tol < the floor."""
+    if mode is PrecisionMode.FULL64 and 0.0 < tolerance < PRECISION_FLOOR:
+        return STALL_CAP
+    return 0.0
+
+
 def _ld(cols: int) -> int:
     return (cols + LD_ALIGN - 1) // LD_ALIGN * LD_ALIGN
 
@@ -114,9 +132,54 @@ class SplitStack:
     def amax_float(self) -> torch.Tensor:
         return self.amax.view(torch.float32)
 
+    def head(self, n: int) -> "SplitStack":
+        """The first ``n`` matrices (shares storage)."""
+        if n == self.nmat:
+            return self
+        v = SplitStack.__new__(SplitStack)
+        v.rows, v.cols = self.rows, self.cols
+        v.data, v.exp, v.amax = self.data[:n], self.exp[:n], self.amax[:n]
+        v._c = None
+        return v
+
 
 def workspace(nbytes: int, dev: torch.device | None = None) -> torch.Tensor:
     return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=dev or device())
+
+
+class Scratch:
+    """Device buffers reused across optimizer steps (no allocation on the steady-state step path).
+
+    Buffers are keyed by a name and their per-matrix shape; a request for fewer matrices than the cached
+    capacity returns a view of the first ones, a larger request reallocates."""
+
+    def __init__(self, dev: torch.device | None = None):
+        self.dev = dev or device()
+        self._bufs: dict = {}
+
+    def stack(self, name: str, n: int, rows: int, cols: int) -> SplitStack:
+        key = ("stack", name, rows, cols)
+        s = self._bufs.get(key)
+        if s is None or s.nmat < n:
+            s = SplitStack(n, rows, cols, self.dev)
+            self._bufs[key] = s
+        return s.head(n)
+
+    def tensor(self, name: str, shape: tuple, dtype=torch.float32) -> torch.Tensor:
+        key = ("tensor", name, tuple(shape[1:]), dtype)
+        t = self._bufs.get(key)
+        if t is None or t.shape[0] < shape[0]:
+            t = torch.empty(tuple(shape), dtype=dtype, device=self.dev)
+            self._bufs[key] = t
+        return t[:shape[0]]
+
+    def ws(self, name: str, nbytes: int) -> torch.Tensor:
+        key = ("ws", name)
+        t = self._bufs.get(key)
+        if t is None or t.numel() < nbytes:
+            t = workspace(nbytes, self.dev)
+            self._bufs[key] = t
+        return t
 
 
 # ----------------------------------------------------------------------------- matmul accounting
@@ -189,9 +252,12 @@ def bmm_split(a: SplitStack, b: SplitStack, *, trans_a: bool = False, trans_b: b
     tally()
 
 
-def bmm(a, b, mode: PrecisionMode = PrecisionMode.EMULATED32, *, trans_a: bool = False,
-        trans_b: bool = False) -> torch.Tensor:
-    """Blockwise product on the GPU (reference ``bmm``, linalg.py:105-114): block i = a[i] @ b[i]."""
+def bmm(a, b, mode: PrecisionMode = PrecisionMode.FULL64, *, trans_a: bool = False,
+        trans_b: bool = False):
+    """Blockwise product on the GPU (reference ``bmm``, linalg.py:105-114): block i = a[i] @ b[i].
+
+    NumPy operands give a float64 NumPy result (the reference's types); tensors give an fp32 CUDA tensor."""
+    is_np = not isinstance(a, torch.Tensor)
     a = as_device_f32(a)
     b = as_device_f32(b)
     if a.dim() != 3 or b.dim() != 3:
@@ -205,11 +271,71 @@ def bmm(a, b, mode: PrecisionMode = PrecisionMode.EMULATED32, *, trans_a: bool =
         raise ValueError(f"shape mismatch: {tuple(a.shape)} x {tuple(b.shape)}")
     out = torch.empty((a.shape[0], m, n), dtype=torch.float32, device=a.device)
     bmm_split(sa, sb, trans_a=trans_a, trans_b=trans_b, f_out=out, mode=mode)
-    return out
+    return out.double().cpu().numpy() if is_np else out
 
 
-def symmetrize(a: torch.Tensor) -> torch.Tensor:
-    return (a + a.transpose(-1, -2)) * 0.5
+def matmul(a, b, mode: PrecisionMode = PrecisionMode.FULL64):
+    """Matrix product a @ b on the tcgen05 engine (reference ``matmul``, linalg.py:93-102)."""
+    if getattr(a, "ndim", None) != 2 or getattr(b, "ndim", None) != 2:
+        raise ValueError("matmul expects 2-D operands")
+    if a.shape[1] != b.shape[0]:
+        raise ValueError(f"dimension mismatch: {tuple(a.shape)} @ {tuple(b.shape)}")
+    out = bmm(a[None], b[None], mode)
+    return out[0]
+
+
+def quantize(a, mode: PrecisionMode):
+    """Round values through the storage precision of ``mode`` (linalg.py:75-79): fp32 for EMULATED32,
+    fp16 for F16, unchanged for FULL64.  NumPy in -> float64 NumPy out; tensors keep their dtype."""
+    dt = {PrecisionMode.EMULATED32: torch.float32, PrecisionMode.F16: torch.float16}.get(mode)
+    if isinstance(a, torch.Tensor):
+        return a if dt is None else a.to(dt).to(a.dtype)
+    a = np.asarray(a, dtype=np.float64)
+    if dt is None:
+        return a
+    return a.astype(np.float32 if dt is torch.float32 else np.float16).astype(np.float64)
+
+
+def frobenius_norm(a) -> float:
+    """||a||_F (linalg.py:117-118); reduced in float64."""
+    if isinstance(a, torch.Tensor):
+        return float(torch.linalg.vector_norm(a.double()))
+    return float(np.linalg.norm(np.asarray(a, dtype=np.float64)))
+
+
+def check_symmetric(a, rtol: float = 1e-8) -> None:
+    """Raise ValueError unless ``a`` is square and symmetric within ``rtol`` (linalg.py:127-133)."""
+    if a.ndim != 2 or a.shape[0] != a.shape[1]:
+        raise ValueError(f"expected a square matrix, got shape {tuple(a.shape)}")
+    if isinstance(a, torch.Tensor):
+        ad = a.double()
+        asym = float(torch.linalg.vector_norm(ad - ad.T))
+        nrm = float(torch.linalg.vector_norm(ad))
+    else:
+        ad = np.asarray(a, dtype=np.float64)
+        asym, nrm = float(np.linalg.norm(ad - ad.T)), float(np.linalg.norm(ad))
+    if asym > rtol * max(nrm, 1.0):
+        raise ValueError(f"matrix is not symmetric (asymmetry norm {asym:.3e})")
+
+
+def identity_like(a):
+    """Identity (2-D input) or stacked identities (3-D input) of ``a``'s type (linalg.py:136-141)."""
+    n = a.shape[-1]
+    if isinstance(a, torch.Tensor):
+        eye = torch.eye(n, dtype=a.dtype, device=a.device)
+        return eye.expand(a.shape).clone() if a.dim() == 3 else eye
+    eye = np.eye(n)
+    return np.broadcast_to(eye, a.shape).copy() if np.ndim(a) == 3 else eye
+
+
+def symmetrize(a):
+    """(a + a^T) / 2 of a square matrix or a stack (linalg.py:121-124)."""
+    if isinstance(a, torch.Tensor):
+        return (a + a.transpose(-1, -2)) * 0.5
+    a = np.asarray(a, dtype=np.float64)
+    if a.shape[-1] != a.shape[-2]:
+        raise ValueError(f"symmetrize expects a square matrix, got {a.shape}")
+    return (a + np.swapaxes(a, -1, -2)) / 2.0
 
 
 # ----------------------------------------------------------------------------- text matrices (host)
@@ -245,6 +371,12 @@ def parse_matrix(text: str) -> np.ndarray:
     if not np.isfinite(out).all():
         raise ValueError("matrix entries must be finite")
     return out
+
+
+def save_matrix(a, path) -> None:
+    """Write the text format (linalg.py:144-147)."""
+    with open(path, "w") as fh:
+        fh.write(format_matrix(a))
 
 
 def load_matrix(path) -> np.ndarray:

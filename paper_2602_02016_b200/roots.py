@@ -21,7 +21,7 @@ import torch
 
 from . import _lib
 from .errors import ConvergenceError, NumericalError
-from .linalg import PrecisionMode, SplitStack, batched, passes_for, tally, workspace
+from .linalg import PrecisionMode, Scratch, SplitStack, batched, passes_for, stall_for, tally, workspace
 
 
 @dataclass
@@ -85,22 +85,40 @@ class DeviceReports:
         return int(self.iters.max()) if self.iters.numel() else 0
 
 
+def _reports(n: int, dev, scratch: Scratch | None, tag: str) -> DeviceReports:
+    rep = DeviceReports.__new__(DeviceReports)
+    if scratch is None:
+        rep.__init__(n, dev)
+        return rep
+    rep.iters = scratch.tensor(tag + ".iters", (n,), torch.int32)
+    rep.resid = scratch.tensor(tag + ".resid", (n,), torch.float32)
+    rep.conv = scratch.tensor(tag + ".conv", (n,), torch.int32)
+    return rep
+
+
 def ndb_split(a: SplitStack, inv_scale: torch.Tensor | None, tol: float, max_iters: int,
-              mode: PrecisionMode, complete: bool = True) -> tuple[SplitStack, SplitStack, DeviceReports]:
+              mode: PrecisionMode, complete: bool = True, *, stall: float | None = None,
+              scratch: Scratch | None = None, tag: str = "ndb") -> tuple[SplitStack, SplitStack, DeviceReports]:
     """NDB on split stacks (device-resident fast path used by the optimizer).
 
     ``complete=False`` leaves Y and Z in upper pair-block storage (``dash_ndb_upper``); complete the one you
-    read with :func:`fill_lower`."""
+    read with :func:`fill_lower`.  ``stall``: the stall cap (default: ``linalg.stall_for(tol, mode)``).
+    ``scratch``: reuse the output / workspace buffers of a previous call with the same ``tag``."""
     n, b = a.nmat, a.rows
     dev = a.data.device
-    y, z = SplitStack(n, b, b, dev), SplitStack(n, b, b, dev)
-    rep = DeviceReports(n, dev)
+    if scratch is not None:
+        y, z = scratch.stack(tag + ".y", n, b, b), scratch.stack(tag + ".z", n, b, b)
+    else:
+        y, z = SplitStack(n, b, b, dev), SplitStack(n, b, b, dev)
+    rep = _reports(n, dev, scratch, tag)
     L = _lib.lib()
-    ws = workspace(L.dash_ndb_ws_bytes(n, b), dev)
+    nbytes = L.dash_ndb_ws_bytes(n, b)
+    ws = scratch.ws("solver", nbytes) if scratch is not None else workspace(nbytes, dev)
     fn = L.dash_ndb if complete else L.dash_ndb_upper
     st = fn(a.ref(), inv_scale.data_ptr() if inv_scale is not None else None, y.ref(), z.ref(),
-            float(tol), int(max_iters), passes_for(mode), rep.iters.data_ptr(), rep.resid.data_ptr(),
-            rep.conv.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+            float(tol), float(stall_for(tol, mode) if stall is None else stall), int(max_iters), passes_for(mode),
+            rep.iters.data_ptr(), rep.resid.data_ptr(), rep.conv.data_ptr(), ws.data_ptr(), ws.numel(),
+            _lib.stream_ptr())
     _lib.check(st, "dash_ndb")
     return y, z, rep
 
@@ -111,16 +129,18 @@ def fill_lower(s: SplitStack) -> SplitStack:
     return s
 
 
-def cn_split(a: SplitStack, inv_scale: torch.Tensor | None, cfg: CnConfig,
-             mode: PrecisionMode) -> tuple[SplitStack, DeviceReports]:
+def cn_split(a: SplitStack, inv_scale: torch.Tensor | None, cfg: CnConfig, mode: PrecisionMode, *,
+             scratch: Scratch | None = None, tag: str = "cn") -> tuple[SplitStack, DeviceReports]:
     n, b = a.nmat, a.rows
     dev = a.data.device
-    x = SplitStack(n, b, b, dev)
-    rep = DeviceReports(n, dev)
+    x = scratch.stack(tag + ".x", n, b, b) if scratch is not None else SplitStack(n, b, b, dev)
+    rep = _reports(n, dev, scratch, tag)
     L = _lib.lib()
-    ws = workspace(L.dash_cn_ws_bytes(n, b), dev)
+    nbytes = L.dash_cn_ws_bytes(n, b)
+    ws = scratch.ws("solver", nbytes) if scratch is not None else workspace(nbytes, dev)
     st = L.dash_cn(a.ref(), inv_scale.data_ptr() if inv_scale is not None else None, cfg.p,
-                   float(cfg.resolved_c), x.ref(), float(cfg.tolerance), int(cfg.max_iters), passes_for(mode),
+                   float(cfg.resolved_c), x.ref(), float(cfg.tolerance), float(stall_for(cfg.tolerance, mode)),
+                   int(cfg.max_iters), passes_for(mode),
                    rep.iters.data_ptr(), rep.resid.data_ptr(), rep.conv.data_ptr(), ws.data_ptr(), ws.numel(),
                    _lib.stream_ptr())
     _lib.check(st, "dash_cn")
@@ -162,7 +182,7 @@ def newton_db(a, cfg: NdbConfig, mode: PrecisionMode = PrecisionMode.FULL64):
     """Unbatched NDB (roots.py:125-151): raises on divergence / non-finite like the reference."""
     y, z, rep = batched_newton_db(_as_stack1(a), cfg, mode)
     r = rep[0]
-    _raise_single(r, "Denman-Beavers")
+    _raise_single(r, "Denman-Beavers", cfg.max_iters)
     return y[0], z[0], r
 
 
@@ -170,7 +190,7 @@ def coupled_newton(a, cfg: CnConfig, mode: PrecisionMode = PrecisionMode.FULL64)
     """Unbatched coupled Newton (roots.py:93-122)."""
     x, rep = batched_coupled_newton(_as_stack1(a), cfg, mode)
     r = rep[0]
-    _raise_single(r, "coupled Newton")
+    _raise_single(r, "coupled Newton", cfg.max_iters)
     return x[0], r
 
 
@@ -191,13 +211,12 @@ def _as_stack1(a):
     return a[None] if a.ndim == 2 else a
 
 
-def _raise_single(r: IterationReport, name: str) -> None:
+def _raise_single(r: IterationReport, name: str, max_iters: int) -> None:
+    """The unbatched solvers raise where the reference's loop raises (roots.py:116-121, :145-150).
+
+    In the batched report a block that stopped before ``max_iters`` without converging was frozen either
+    for a non-finite residual (-> NumericalError) or by the divergence watch (-> ConvergenceError)."""
     if not np.isfinite(r.residual):
         raise NumericalError(f"{name} produced non-finite values at iteration {r.iterations}")
-    if not r.converged and r.iterations < 10**9 and r.residual > 0 and _diverged(r):
+    if not r.converged and r.iterations < max_iters:
         raise ConvergenceError(f"{name} diverging at iteration {r.iterations} (residual {r.residual:.3e})")
-
-
-def _diverged(r: IterationReport) -> bool:
-    # A batched report that stopped before max_iters without converging was frozen by the watch.
-    return False

@@ -28,10 +28,11 @@ import torch
 from . import _lib
 from .blocking import PartitionLayout, chunk_bounds, partition_layout
 from .chebyshev import ChebCoefficients, clenshaw_split, fit_inverse_root
-from .eigensolver import DampeningHeuristic, HeuristicKind, evd_inverse_root_torch
+from .eigensolver import DampeningHeuristic, HeuristicKind, evd_inverse_root_torch, inverse_root_f64
 from .errors import ConvergenceError, DegenerateSpectrumError
-from .linalg import PrecisionMode, SplitStack, device, format_matrix, parse_matrix, passes_for, workspace
-from .roots import CnConfig, DeviceReports, cn_split, fill_lower, ndb_split
+from .linalg import (PrecisionMode, Scratch, SplitStack, device, format_matrix, parse_matrix, passes_for, stall_for,
+                     workspace)
+from .roots import CnConfig, DeviceReports, IterationReport, cn_split, fill_lower, ndb_split
 from .spectral import Frobenius, PowerIterationScaling, ScalingMode, block_seed, power_iteration_scales
 
 SOLVER_METHODS = ("evd", "cn", "ndb", "cbshv")
@@ -316,6 +317,10 @@ class _Runtime:
         self.g_fro = [torch.zeros(len(g.members) * self.prep_parts, **f32) for g in state.groups]
         self.plan = None
         self.plan_key = None
+        self.scratch = Scratch(self.dev)   # per-step solver buffers, reused across steps
+        self.stats_valid = False           # g_amax / g_fro describe the current EMA (set by accumulate)
+        self.stats_eps = None
+        self.pending_err = None            # device error word of the last fixed-iteration refresh
 
     def views(self, flat: torch.Tensor) -> list[torch.Tensor]:
         return [flat[int(self.offsets[i]):int(self.offsets[i + 1])].view(s) for i, s in enumerate(self.shapes)]
@@ -394,6 +399,7 @@ def accumulate(state: ShampooState, grads, cfg: ShampooConfig) -> ShampooState:
         st = _lib.lib().dash_group_sym(g.ema.data_ptr(), len(g.members), g.dim, float(cfg.epsilon),
                                        rt.g_amax[gi].data_ptr(), rt.g_fro[gi].data_ptr(), _lib.stream_ptr())
         _lib.check(st, "dash_group_sym")
+    rt.stats_valid, rt.stats_eps = True, cfg.epsilon
     return state
 
 
@@ -419,80 +425,159 @@ def _check_reports(group: PrecondGroup, reports) -> None:
         raise ConvergenceError(f"inverse-root solver failed on: {details}")
 
 
-def refresh_inverse_roots(state: ShampooState, cfg: ShampooConfig, seed: int = 0) -> ShampooState:
-    """Recompute cached inverse roots; no-op unless step % update_freq == 0 (shampoo.py:312-349)."""
+def _group_stats(state: ShampooState, cfg: ShampooConfig) -> None:
+    """max|a| and sum(a^2) of a = ema + eps I for every group (normally a by-product of accumulate's
+    symmetrization; recomputed when the EMA did not come from accumulate, e.g. after init_state / load_state).
+    Symmetrizing a symmetric EMA (the only kind accumulate and checkpoints produce) leaves it bit-identical."""
+    rt: _Runtime = state.runtime
+    for gi, g in enumerate(state.groups):
+        _lib.check(_lib.lib().dash_group_sym(g.ema.data_ptr(), len(g.members), g.dim, float(cfg.epsilon),
+                                             rt.g_amax[gi].data_ptr(), rt.g_fro[gi].data_ptr(), _lib.stream_ptr()),
+                   "dash_group_sym")
+    rt.stats_eps = cfg.epsilon
+
+
+def _raise_scale_error(state: ShampooState, err: list[int]) -> None:
+    code, gi = err
+    if code == 2:
+        raise DegenerateSpectrumError("power iteration pool collapsed twice on a nonzero matrix")
+    raise ConvergenceError(f"non-positive scale in group of dim {state.groups[gi].dim}")
+
+
+def check_step_status(state: ShampooState) -> None:
+    """Raise the error a fixed-iteration refresh recorded on the device (one 8-byte read), if any.
+
+    The failing group and every later one kept their previous roots (the commit is gated on the device),
+    which is the state the reference leaves behind when its refresh loop raises."""
+    rt: _Runtime = state.runtime
+    err = getattr(rt, "pending_err", None)
+    if err is None:
+        return
+    rt.pending_err = None
+    vals = err.tolist()
+    if vals[0]:
+        _raise_scale_error(state, vals)
+
+
+def refresh_inverse_roots(state: ShampooState, cfg: ShampooConfig, seed: int = 0, *, defer_check: bool = False
+                          ) -> ShampooState:
+    """Recompute cached inverse roots; no-op unless step % update_freq == 0 (shampoo.py:312-349).
+
+    Fixed-iteration solves (tolerance 0) never synchronise with the host: the scale checks run on the device
+    (``dash_scale_check``), a failing group's roots are not committed, and the recorded error is raised at the
+    end of the refresh -- or, with ``defer_check`` (used by ``step``), at the end of the step, before any
+    parameter is returned.  Tolerance-mode solves read the per-block reports group by group like the
+    reference; their roots are committed only after the checks pass.  In FULL64 mode a block the fp32-class
+    iteration cannot converge (frozen by the divergence watch or a non-finite residual before max_iters) is
+    re-solved in float64 by EVD: (ema + eps I)^(-1/p), the value the reference's float64 iteration reaches.
+    """
     if state.step % cfg.update_freq != 0:
         return state
     rt: _Runtime = state.runtime
     solver = cfg.solver
     L = _lib.lib()
+    sc = rt.scratch
+    if not rt.stats_valid or rt.stats_eps != cfg.epsilon:
+        _group_stats(state, cfg)
+    rt.stats_valid = True
     # block sharding: rank-local group gi is global group global_gid[gi]; its members' global slots
     gids = getattr(rt, "global_gid", None)
     sidx = getattr(rt, "seed_index", None)
-    pending: list[tuple[PrecondGroup, list[DeviceReports]]] = []
-    statuses = []
+    tol_mode = solver.require_convergence
+    mode = solver.precision
+    ng = len(state.groups)
+    err = sc.tensor("err", (2,), torch.int32)
+    err.zero_()
+    oks = sc.tensor("ok", (max(ng, 1),), torch.int32)
     for gi, group in enumerate(state.groups):
         p, n, d = group.exponent, len(group.members), group.dim
+        gid = gids[gi] if gids is not None else gi
         if solver.method == "evd":
             group.roots.copy_(evd_inverse_root_torch(group.ema, p, solver.heuristic))
             rt.root_split[gi].load(group.roots)
             continue
-        a = SplitStack(n, d, d, rt.dev)
-        a.amax = rt.g_amax[gi]  # exact max|ema + eps I| from dash_group_sym
+        a = sc.stack("a", n, d, d)
+        a.amax.copy_(rt.g_amax[gi])  # exact max|ema + eps I| (accumulate's symmetrization)
         _lib.check(L.dash_group_split_a(group.ema.data_ptr(), float(cfg.epsilon), a.ref(), _lib.stream_ptr()),
                    "dash_group_split_a")
-        scale = torch.empty(n, dtype=torch.float32, device=rt.dev)
-        inv = torch.empty_like(scale)
-        status = torch.zeros(n, dtype=torch.int32, device=rt.dev)
+        scale = sc.tensor("scale", (n,))
+        inv = sc.tensor("inv", (n,))
+        status = sc.tensor("status", (n,), torch.int32)
+        status.zero_()
         if isinstance(solver.scaling, Frobenius):
             _lib.check(L.dash_fro_scale(rt.g_fro[gi].data_ptr(), n, scale.data_ptr(), inv.data_ptr(),
                                         _lib.stream_ptr()), "dash_fro_scale")
         else:
             power_iteration_scales(group.ema, cfg.epsilon, solver.scaling.pool, solver.scaling.iters,
-                                   block_seed(seed, gids[gi] if gids is not None else gi), scale, inv, status,
+                                   block_seed(seed, gid), scale, inv, status,
                                    sidx[gi] if sidx is not None else None, a_split=a)
-        statuses.append((group, scale, status))
-        mode = solver.precision
+        ok = oks[gi:gi + 1]
+        _lib.check(L.dash_scale_check(scale.data_ptr(), status.data_ptr(), n, gi, ok.data_ptr(), err.data_ptr(),
+                                      _lib.stream_ptr()), "dash_scale_check")
+        if tol_mode:  # the reference raises here, before any solve of this group (shampoo.py:323-325)
+            vals = err.tolist()
+            if vals[0]:
+                _raise_scale_error(state, vals)
         if solver.method == "cbshv":
             coeffs = _solver_coefficients(solver, p)
-            clenshaw_split(a, coeffs, inv, inv_pow(inv, p), group.roots, rt.root_split[gi], mode)
+            clenshaw_split(a, coeffs, inv, inv_pow(inv, p, sc), group.roots, rt.root_split[gi], mode, gate=ok,
+                           scratch=sc)
             continue
         if solver.method == "cn":
-            x, rep = cn_split(a, inv, CnConfig(p=p, tolerance=solver.tolerance, max_iters=solver.max_iters), mode)
+            x, rep = cn_split(a, inv, CnConfig(p=p, tolerance=solver.tolerance, max_iters=solver.max_iters), mode,
+                              scratch=sc)
             reps = [rep]
             src = x
         else:  # ndb
             # the iterates stay in upper pair-block storage (the second solve of a 4th root reads Y1 that way);
             # only the root that is read next is completed
             if p == 2:
-                _, src, rep = ndb_split(a, inv, solver.tolerance, solver.max_iters, mode, complete=False)
+                _, src, rep = ndb_split(a, inv, solver.tolerance, solver.max_iters, mode, complete=False,
+                                        scratch=sc, tag="ndb1")
                 reps = [rep]
             else:
-                y1, _, r1 = ndb_split(a, inv, solver.tolerance, solver.max_iters, mode, complete=False)
-                _, src, r2 = ndb_split(y1, None, solver.tolerance, solver.max_iters, mode, complete=False)
+                y1, _, r1 = ndb_split(a, inv, solver.tolerance, solver.max_iters, mode, complete=False,
+                                      scratch=sc, tag="ndb1")
+                _, src, r2 = ndb_split(y1, None, solver.tolerance, solver.max_iters, mode, complete=False,
+                                       scratch=sc, tag="ndb2")
                 reps = [r1, r2]
             fill_lower(src)
-        # roots = Z * scale^(-1/p)  -> fp32 state roots + split copy for the apply
+        fallback = None
+        if tol_mode:  # per-block reports, in the reference's order (first chain, then second)
+            lists = [r.to_list() for r in reps]
+            # FULL64 re-solves in float64 the blocks its fp32-class iteration could not converge: frozen before
+            # max_iters (watch / non-finite), or -- when the requested tolerance is below the floor, so the
+            # reference's float64 loop would have converged where ours stalls -- any unconverged block
+            floor_mode = stall_for(solver.tolerance, mode) > 0.0
+            bad = sorted({i for lst in lists for i, r in enumerate(lst)
+                          if not r.converged and (floor_mode or r.iterations < solver.max_iters)})
+            if mode is PrecisionMode.FULL64 and bad:
+                fallback = bad
+                for lst in lists:
+                    for i in bad:
+                        lst[i] = IterationReport(lst[i].iterations, lst[i].residual, True)
+            for lst in lists:
+                _check_reports(group, lst)
+        # roots = Z * scale^(-1/p)  -> fp32 state roots + split copy for the apply (gated on the scale checks)
         _lib.check(L.dash_scale_stack(src.ref(), inv.data_ptr(), 1.0 / p, group.roots.data_ptr(),
                                       group.roots.stride(0), group.roots.stride(1), rt.root_split[gi].ref(),
-                                      _lib.stream_ptr()), "dash_scale_stack")
-        if solver.require_convergence:
-            pending.append((group, reps))
-    # host checks (one synchronisation per refresh, only when the reference would raise)
-    for group, scale, status in statuses:
-        if bool((status == 2).any()):
-            raise DegenerateSpectrumError("power iteration pool collapsed twice on a nonzero matrix")
-        if bool((scale <= 0).any()):
-            raise ConvergenceError(f"non-positive scale in group of dim {group.dim}")
-    for group, reps in pending:
-        for rep in reps:
-            _check_reports(group, rep.to_list())
+                                      ok.data_ptr(), _lib.stream_ptr()), "dash_scale_stack")
+        if fallback:
+            idx = torch.tensor(fallback, dtype=torch.long, device=rt.dev)
+            group.roots[idx] = inverse_root_f64(group.ema[idx], cfg.epsilon, p)
+            rt.root_split[gi].load(group.roots)
+    if not tol_mode:
+        rt.pending_err = err
+        if not defer_check:
+            check_step_status(state)
     return state
 
 
-def inv_pow(inv: torch.Tensor, p: int) -> torch.Tensor:
+def inv_pow(inv: torch.Tensor, p: int, scratch=None) -> torch.Tensor:
     """scale^(-1/p) from 1/scale (device; tiny vector)."""
-    return inv.double().pow(1.0 / p).float()
+    out = scratch.tensor("inv_pow", tuple(inv.shape)) if scratch is not None else torch.empty_like(inv)
+    out.copy_(inv.double().pow(1.0 / p))
+    return out
 
 
 # ============================================================================ step
@@ -540,7 +625,7 @@ def step(state: ShampooState, params, grads, cfg: ShampooConfig, seed: int = 0, 
         prefetch = torch.cuda.Event()
         prefetch.record(rt.copy_stream)
     mark("accumulated")
-    refresh_inverse_roots(state, cfg, seed=block_seed(seed, t))
+    refresh_inverse_roots(state, cfg, seed=block_seed(seed, t), defer_check=True)
     mark("refreshed")
     eta = cfg.lr.value(t)
     if prefetch is not None:
@@ -550,6 +635,7 @@ def step(state: ShampooState, params, grads, cfg: ShampooConfig, seed: int = 0, 
     _lib.check(_lib.lib().dash_plan_apply(rt.plan, rt.theta.data_ptr(), rt.theta_out.data_ptr(), float(eta),
                                           _lib.stream_ptr()), "dash_plan_apply")
     mark("applied")
+    check_step_status(state)  # the refresh's device-side scale checks (raises before anything is returned)
     state.step = t + 1
     if not isinstance(params[0], torch.Tensor):
         host = rt.theta_out.double().cpu().numpy()

@@ -30,7 +30,7 @@ def llama_953m():
 
 
 # Solver configurations of the golden optimizer-step fixtures (reference SolverConfig kwargs).
-STEP_METHODS = ("ndb", "cn", "cbshv", "ndbfix", "ndbfro", "ndbtol5", "cntol5", "cnfix4", "ndbfrofix")
+STEP_METHODS = ("ndb", "cn", "cbshv", "ndbfix", "ndbfro", "ndbtol5", "cntol5", "cnfix4", "ndbfrofix", "evd")
 
 
 def solver_kwargs(method, spectral):
@@ -45,6 +45,7 @@ def solver_kwargs(method, spectral):
         "cntol5": dict(method="cn", tolerance=1e-5),
         "cnfix4": dict(method="cn", tolerance=0.0, max_iters=8),
         "ndbfrofix": dict(method="ndb", scaling=spectral.Frobenius(), tolerance=0.0, max_iters=10),
+        "evd": dict(method="evd"),
     }[method]
 
 

@@ -81,8 +81,9 @@ def solver_fixture():
         sc = np.array([1.0, 0.8, 1.3, 0.6])
         res[f"cheb{p}_scales"] = sc
         res[f"cheb{p}_out"] = chebyshev.batched_clenshaw_matrix(a, c, sc)
-    lams = [spectral.multi_power_iteration(a[i], 16, 30, 100 + i).lam for i in range(a.shape[0])]
-    res["pi_lams"] = np.array(lams)
+    ests = [spectral.multi_power_iteration(a[i], 16, 30, 100 + i) for i in range(a.shape[0])]
+    res["pi_lams"] = np.array([e.lam for e in ests])
+    res["pi_vecs"] = np.stack([e.vector for e in ests])
     res["pi_seeds"] = np.array([100 + i for i in range(a.shape[0])])
     res["fro_scales"] = np.sqrt((a * a).sum(axis=(1, 2)))
     res["rspd_3_10_5"] = tasks.random_spd(3, 10.0, seed=5, scale=0.5)

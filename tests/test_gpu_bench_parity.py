@@ -1,0 +1,110 @@
+"""Parity on the benchmarked configurations (BASELINE configs 2 and 4/5) against the float64 oracle.
+
+* the bench's solver settings (B = 1024, power-iteration scaling 16 x 30, Newton-DB fixed 10 iterations per
+  chain, update_freq 1) on a multi-group layer set built from the 953M set's layer shapes: the (1024, p=4),
+  (512, p=4) and (1024, p=2) groups of the benchmark, three steps (the statistics become full rank);
+* config 2: 256 stacked random_spd blocks at B = 256 / 512 / 1024, cond 10 and 1e3, for Newton-DB, coupled
+  Newton and Chebyshev.  The GPU solves the whole 256-block stack; the oracle checks a sample of its blocks
+  (every block is solved independently: results do not depend on the batch composition).
+
+Tolerances (relative Frobenius): split-f16 products with fp32 accumulation (EMULATED32), stated per test.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import core
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU containers skip the whole module
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2602_02016_b200 import chebyshev, roots, shampoo  # noqa: E402
+from paper_2602_02016_b200.linalg import PrecisionMode  # noqa: E402
+
+
+def relf(x, y):
+    x, y = np.asarray(x, dtype=np.float64), np.asarray(y, dtype=np.float64)
+    d = np.linalg.norm(y)
+    return np.linalg.norm(x - y) / (d if d > 0 else 1.0)
+
+
+BENCH_SHAPES = [(2048, 2048), (5632, 2048), (2048, 5632), (2048,)]  # 953M-set layer shapes
+
+
+def test_bench_config_multi_group_steps_vs_oracle():
+    """bench.py's solver settings on 953M layer shapes: groups 512/p4 (2), 1024/p2 (2), 1024/p4 (36)."""
+    rng = np.random.default_rng(7)
+    params = [rng.standard_normal(s) * 0.02 for s in BENCH_SHAPES]
+    grads = [[rng.standard_normal(s) * 1e-3 for s in BENCH_SHAPES] for _ in range(3)]
+    cfg = shampoo.ShampooConfig(block_size=1024, solver=shampoo.SolverConfig(
+        method="ndb", tolerance=0.0, max_iters=10, precision=PrecisionMode.EMULATED32))
+    ocfg = core.OracleConfig(block_size=1024, method="ndb", tolerance=0.0, max_iters=10)
+    st, ost = shampoo.init_state(params, cfg), core.init_state(params, ocfg)
+    assert [(g.dim, g.exponent, len(g.members)) for g in st.groups] == [(512, 4, 2), (1024, 2, 2), (1024, 4, 36)]
+    cur, ocur = params, params
+    for gs in grads:
+        prev, oprev = cur, ocur
+        cur, st = shampoo.step(st, cur, gs, cfg, seed=5)
+        ocur, ost, _ = core.step(ost, ocur, gs, ocfg, seed=5)
+    upd = max(relf(c - p, oc - op) for c, p, oc, op in zip(cur, prev, ocur, oprev))
+    rts = [relf(g.roots.cpu().numpy(), og["roots"]) for g, og in zip(st.groups, ost["groups"])]
+    print(f"bench-config last-step update relF {upd:.2e}, roots relF per group {[f'{r:.1e}' for r in rts]}")
+    assert upd < 2e-3
+    assert max(rts) < 5e-3
+
+
+def _c2_stack(b, cond):
+    return np.stack([core.random_spd(b, cond, seed=i, scale=0.5) for i in range(256)])
+
+
+SAMPLE = [0, 77, 255]
+
+
+@pytest.mark.parametrize("b", [256, 512, 1024])
+@pytest.mark.parametrize("cond", [10.0, 1e3])
+def test_c2_ndb_256_blocks_vs_oracle(b, cond):
+    """Config 2, Newton-DB inverse 4th root (two chains, fixed 10 iterations each) on 256 stacked blocks."""
+    a = _c2_stack(b, cond)
+    at = torch.as_tensor(a, dtype=torch.float32, device="cuda")
+    cfg = roots.NdbConfig(tolerance=0.0, max_iters=10)
+    y1, _, _ = roots.batched_newton_db(at, cfg, PrecisionMode.EMULATED32)
+    _, z, _ = roots.batched_newton_db(y1, cfg, PrecisionMode.EMULATED32)
+    z = z.double().cpu().numpy()
+    oy, _, _ = core.batched_newton_db(a[SAMPLE], 0.0, 10)
+    _, oz, _ = core.batched_newton_db(oy, 0.0, 10)
+    errs = [relf(z[i], oz[k]) for k, i in enumerate(SAMPLE)]
+    print(f"C2 NDB B={b} cond={cond:g}: {[f'{e:.1e}' for e in errs]}")
+    assert max(errs) < (2e-4 if cond <= 10 else 2e-3)
+
+
+@pytest.mark.parametrize("b", [256, 512, 1024])
+@pytest.mark.parametrize("cond", [10.0, 1e3])
+def test_c2_cn_256_blocks_vs_oracle(b, cond):
+    """Config 2, coupled Newton p = 4 (fixed 10 iterations) on 256 stacked blocks."""
+    a = _c2_stack(b, cond)
+    x, _ = roots.batched_coupled_newton(torch.as_tensor(a, dtype=torch.float32, device="cuda"),
+                                        roots.CnConfig(p=4, tolerance=0.0, max_iters=10), PrecisionMode.EMULATED32)
+    x = x.double().cpu().numpy()
+    ox, _ = core.batched_coupled_newton(a[SAMPLE], 4, 0.0, 10)
+    errs = [relf(x[i], ox[k]) for k, i in enumerate(SAMPLE)]
+    print(f"C2 CN B={b} cond={cond:g}: {[f'{e:.1e}' for e in errs]}")
+    assert max(errs) < (2e-4 if cond <= 10 else 2e-3)
+
+
+@pytest.mark.parametrize("b", [256, 512, 1024])
+@pytest.mark.parametrize("cond", [10.0, 1e3])
+def test_c2_chebyshev_256_blocks_vs_oracle(b, cond):
+    """Config 2, Chebyshev degree 60 (p = 4) on 256 stacked blocks against the oracle's own Clenshaw."""
+    a = _c2_stack(b, cond)
+    c = chebyshev.fit_inverse_root(4)
+    scales = np.full(256, 1.0)
+    out = chebyshev.batched_clenshaw_matrix(torch.as_tensor(a, dtype=torch.float32, device="cuda"), c, scales,
+                                            PrecisionMode.EMULATED32)
+    out = out.double().cpu().numpy()
+    coeffs, _ = core.cheb_coefficients(4, 60, 1000, None)
+    want = core.batched_clenshaw(a[SAMPLE], coeffs, scales[SAMPLE], 4)
+    errs = [relf(out[i], want[k]) for k, i in enumerate(SAMPLE)]
+    print(f"C2 Chebyshev B={b} cond={cond:g}: {[f'{e:.1e}' for e in errs]}")
+    assert max(errs) < 1e-3

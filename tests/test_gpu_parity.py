@@ -62,19 +62,6 @@ def test_device_pcg64_matches_numpy(seed):
     np.testing.assert_array_equal(got, want)
 
 
-def test_power_iteration_vs_golden(golden):
-    g = golden["solvers"]
-    a = g["a"]
-    for i, s in enumerate(g["pi_seeds"].tolist()):
-        est = spectral.batched_multi_power_iteration(a[i:i + 1], 16, 30, 0)  # seed is per call below
-        del est
-    # the reference draws block i's pool from block_seed(seed, i); golden used plain seeds -> compare via
-    # single-block calls whose child seed equals the golden seed is not possible, so check lambda_max bound:
-    lams = np.array([e.lam for e in spectral.batched_multi_power_iteration(a, 16, 30, 7)])
-    true = np.linalg.eigvalsh(a)[:, -1]
-    assert np.all(lams <= true * (1 + 1e-5)) and np.all(lams >= true * 0.99)
-
-
 def test_power_iteration_bitexact_seeds_vs_oracle():
     rng = np.random.default_rng(3)
     a = np.stack([core.random_spd(96, c, seed=i, scale=s) for i, (c, s) in enumerate([(10, 0.5), (1e3, 2.0), (50, 1e-3)])])
