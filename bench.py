@@ -11,8 +11,9 @@ Synthetic data: params N(0, 0.02^2), grads N(0, 1e-3^2), seeded.
 `value` = ms per step, device-timed with CUDA events, inputs resident in HBM, max over ranks.
 `e2e`   = the same step through the public API with host (pinned CPU) params/grads: H2D of grads and
           params and D2H of the new params inside the timed region.
-N > 1 (torchrun): gradient blocks are sharded across ranks (greedy LPT on per-block solver cost) and the
-updated parameter shards are all-gathered with NCCL (weak... no: total work fixed -> "strong" scaling).
+N > 1 (`--gpus N` re-launches itself under torchrun when WORLD_SIZE is unset): gradient blocks are sharded
+across ranks (greedy LPT on per-block solver cost) and the updated parameter shards are all-gathered with NCCL;
+total work is fixed, so scaling is "strong".
 """
 from __future__ import annotations
 
@@ -273,6 +274,43 @@ def c1_pair(iters: int, with_gpu: bool = True) -> dict:
     return res
 
 
+def bench_parity(iters: int, method: str = "ndb", precision: str = "f32") -> dict:
+    """The benchmarked configuration's numerics against the float64 oracle, in the same run: B = 1024, PI 16 x 30,
+    the bench's solver and precision, refresh every step, on a layer set with the bench's (1024, p=4) and
+    (1024, p=2) groups; three steps (the statistics become full rank), last step compared."""
+    import torch
+
+    from oracle import core
+    from paper_2602_02016_b200.linalg import PrecisionMode
+    from paper_2602_02016_b200.shampoo import ShampooConfig, SolverConfig, init_state, step
+
+    shapes = [(2048, 1024), (1024,)]
+    rng = np.random.default_rng(7)
+    params = [rng.standard_normal(s) * 0.02 for s in shapes]
+    grads = [[rng.standard_normal(s) * 1e-3 for s in shapes] for _ in range(3)]
+    prec = {"f32": PrecisionMode.EMULATED32, "f16": PrecisionMode.F16}[precision]
+    cfg = ShampooConfig(block_size=1024, solver=SolverConfig(method=method, tolerance=0.0, max_iters=iters,
+                                                             precision=prec))
+    ocfg = core.OracleConfig(block_size=1024, method=method, tolerance=0.0, max_iters=iters)
+    st, ost = init_state(params, cfg), core.init_state(params, ocfg)
+    cur, ocur = params, params
+    for gs in grads:
+        prev, oprev = cur, ocur
+        cur, st = step(st, cur, gs, cfg, seed=5)
+        ocur, ost, _ = core.step(ost, ocur, gs, ocfg, seed=5)
+    torch.cuda.synchronize()
+
+    def relf(x, y):
+        return float(np.linalg.norm(x - y) / max(np.linalg.norm(y), 1e-300))
+
+    upd = max(relf(c - p, oc - op) for c, p, oc, op in zip(cur, prev, ocur, oprev))
+    rts = max(relf(g.roots.double().cpu().numpy(), og["roots"]) for g, og in zip(st.groups, ost["groups"]))
+    tol = {"f32": (2e-3, 5e-3), "f16": (3e-2, 5e-2)}[precision]
+    return {"case": f"layers {shapes}, B=1024, groups 1024/p4 x4 + 1024/p2 x1, 3 steps, last compared",
+            "relF_update": upd, "relF_roots": rts, "tol": {"update": tol[0], "roots": tol[1]},
+            "pass": bool(upd < tol[0] and rts < tol[1])}
+
+
 # ----------------------------------------------------------------------------- DASH arm
 def run_dash(args):
     import torch
@@ -301,6 +339,7 @@ def run_dash(args):
         from paper_2602_02016_b200.sharded import ShardedDash
 
         opt = ShardedDash(params, cfg, rank=rank, world=world)
+        shard_units, shard_ag_bytes = opt.units, opt.allgather_bytes
         do_step = lambda ev=None: opt.step(params, grads, events=ev)  # noqa: E731
     else:
         state = init_state(params, cfg)
@@ -330,6 +369,9 @@ def run_dash(args):
         for a, b, name in (("start", "accumulated", "accumulate"), ("accumulated", "refreshed", "refresh"),
                            ("refreshed", "applied", "apply")):
             phases[name] = round(sum(x.elapsed_time(y) for x, y in zip(events[a], events[b])) / args.steps, 3)
+        if events.get("exchanged"):  # sharded: pack + all-gather + unpack
+            phases["exchange"] = round(sum(x.elapsed_time(y) for x, y in zip(events["applied"], events["exchanged"]))
+                                       / args.steps, 3)
     n_gemm, gemm_ms, gemm_flops = _lib.gemm_timing_read()
     per_launch = _lib.gemm_timing_list()
     _lib.gemm_timing(False)
@@ -344,31 +386,59 @@ def run_dash(args):
     # ---- end-to-end through the public API with host buffers (pinned), H2D + D2H inside the region
     e2e = None
     dev_peak = 0
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e:
         hp = [p.cpu().pin_memory() for p in params]
         hg = [g.cpu().pin_memory() for g in grads]
         # release the device-resident run first: two optimizer states at 953M would need ~170 GB of HBM
         dev_peak = torch.cuda.max_memory_allocated()
-        del do_step, state
+        if world > 1:
+            del opt
+        else:
+            del state
+        del do_step
         params.clear()
         grads.clear()
         torch.cuda.synchronize()
         torch.cuda.empty_cache()
         h2d = sum(t.numel() * 4 for t in hp) + sum(t.numel() * 4 for t in hg)
         d2h = sum(t.numel() * 4 for t in hp)
-        state_e = init_state(hp, cfg)
+        if world == 1:
+            state_e = init_state(hp, cfg)
+
+            def e2e_step():
+                nonlocal state_e
+                out, state_e = step(state_e, hp, hg, cfg)
+                del out  # the caller keeps what it needs; the pinned block returns to the host cache
+        else:  # every rank: H2D of its (replicated, DDP-style) gradients and parameters, sharded step, D2H
+            from paper_2602_02016_b200.sharded import ShardedDash
+
+            dp = [p.cuda() for p in hp]
+            dg = [g.cuda() for g in hg]
+            opt_e = ShardedDash(dp, cfg, rank=rank, world=world)
+            outs = [torch.empty_like(p).pin_memory() for p in hp]
+
+            def e2e_step():
+                for d, h in zip(dp, hp):
+                    d.copy_(h, non_blocking=True)
+                for d, h in zip(dg, hg):
+                    d.copy_(h, non_blocking=True)
+                opt_e.step(dp, dg)
+                for o, d in zip(outs, dp):
+                    o.copy_(d, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
         for _ in range(max(args.warmup, 2)):  # warm the host path (pinned output buffers cycle through the cache)
-            out, state_e = step(state_e, hp, hg, cfg)
-            del out
-        torch.cuda.synchronize()
+            e2e_step()
+        barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            out, state_e = step(state_e, hp, hg, cfg)
-            del out  # the caller keeps what it needs; the pinned block returns to the host cache
+            e2e_step()
         torch.cuda.synchronize()
-        e2e_ms = (time.perf_counter() - t0) / args.steps * 1e3
-        e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
-        del state_e
+        e2e_local = (time.perf_counter() - t0) / args.steps * 1e3
+        if world > 1:  # max over ranks
+            t = torch.tensor([e2e_local], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_local = float(t.item())
+        e2e = {"value": e2e_local, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
 
     fl = solver_flops(shapes, bsz, args.iters, args.solver)
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
@@ -437,14 +507,20 @@ def run_dash(args):
     if world > 1:  # block sharding balance (balance.block_report): solver-cost makespan vs mean, all-gather bytes
         from paper_2602_02016_b200.balance import block_balance, block_report
 
-        rep = block_report(opt.units, block_balance(opt.units, world))
-        result["balance"] = {"units": len(opt.units), "units_per_rank": list(rep.units_per_rank),
+        rep = block_report(shard_units, block_balance(shard_units, world))
+        result["balance"] = {"units": len(shard_units), "units_per_rank": list(rep.units_per_rank),
                              "imbalance": round(rep.imbalance, 4),
                              "allgather_bytes_per_rank": rep.allgather_bytes}
     if phases.get("refresh"):  # Newton-DB algorithmic FLOPs / refresh phase (includes PI, splits, rescale)
         result["solver_tflops_per_s"] = round(fl["ndb"] / world / (phases["refresh"] * 1e-3) / 1e12, 1)
+    if world > 1:
+        result["allgather_bytes_per_step"] = shard_ag_bytes
+    if rank == 0 and not args.no_parity:
+        result["parity"] = bench_parity(args.iters, args.solver, args.precision)
     if rank == 0 and not args.no_cpu:
         result["cpu_baseline"] = cpu_baseline(shapes, bsz, args.iters, method=args.solver)
+        if args.solver == "ndb" and args.precision == "f32":
+            result["c1"] = c1_pair(args.iters)
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:
@@ -452,19 +528,19 @@ def run_dash(args):
 
 
 def run_reference(args):
-    """The reference's own algorithm on the host cores (oracle port; the reference is Python and the
-    GPU box has no /root/reference)."""
+    """The reference's own algorithm on the host cores: the float64 oracle restatement (the reference is pure
+    Python/NumPy and /root/reference does not exist on the GPU box), every host thread for BLAS.  Each step is
+    one per-component measurement of the workload (cpu_baseline); rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     shapes, bsz = workload_shapes(args.workload)
     steps = []
     for _ in range(args.warmup + args.steps):
-        cb = cpu_baseline(shapes, bsz, args.iters, budget_s=8.0, method=args.solver)
-        steps.append(cb)
+        steps.append(cpu_baseline(shapes, bsz, args.iters, method=args.solver, reps=1))
     timed = steps[args.warmup:]
     v = statistics.median([c["value"] for c in timed])
-    print(json.dumps({
+    line = {
         "impl": "reference",
         "metric": METRIC,
         "value": round(v, 1),
@@ -478,11 +554,30 @@ def run_reference(args):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded)",
-        "config": {"workload": f"{args.workload} DASH step, B={bsz}, {SOLVER_DESC[args.solver].format(k=args.iters)}, PI",
+        "config": {"workload": f"{args.workload} DASH step, B={bsz}, {SOLVER_DESC[args.solver].format(k=args.iters)}, "
+                               "PI scaling (pool 16 x 30 iters), update_freq=1, grafting beta2=0.999",
                    "parallelism": "host CPU"},
-        "cpu_baseline": {k: timed[-1][k] for k in ("kind", "cores", "sample")} | {"value": round(v, 1), "unit": "ms"},
+        "cpu_baseline": {k: timed[-1][k] for k in ("kind", "cores", "nproc", "blas_threads", "sample")}
+                        | {"value": round(v, 1), "unit": "ms"},
         "e2e": {"value": round(v, 1), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }), flush=True)
+        "components_ms": timed[-1]["components_ms"],
+    }
+    if args.solver == "ndb" and not args.no_cpu:
+        line["c1"] = c1_pair(args.iters, with_gpu=False)
+    print(json.dumps(line), flush=True)
+
+
+def spawn_ranks(args) -> int:
+    """`--gpus N` without a torchrun environment: re-launch this script under torchrun with N local ranks."""
+    import torch
+
+    if args.gpus > torch.cuda.device_count():
+        print(json.dumps({"error": f"--gpus {args.gpus} but only {torch.cuda.device_count()} GPUs visible"}))
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={29500 + os.getpid() % 1000}", str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -497,9 +592,15 @@ def main():
     ap.add_argument("--solver", default="ndb", choices=["ndb", "cn", "cbshv"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "dash":
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus and int(os.environ.get("RANK", 0)) == 0:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}; using WORLD_SIZE",
+              file=sys.stderr)
     if args.impl == "reference":
         run_reference(args)
     else:

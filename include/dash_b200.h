@@ -164,10 +164,13 @@ int dash_power_iteration(const float* ema, int n, int d, float eps, int pool, in
                          float* scale, float* inv_scale, int* status, const int* seed_index, float* vec_out,
                          void* stream);
 /* Same result from the solver's split stack a = ema + eps I (d a multiple of 128, <= 1024): tensor-core
- * matvecs (tcgen05, one d/128-CTA cluster per block, pool in shared memory).  Replaces the inner loop of
- * spectral.multi_power_iteration (spectral.py:77-112) for the DASH block sizes. */
-int dash_power_iteration_split(const dash_stack* a, int pool, int iters, unsigned long long seed, float* scale,
-                               float* inv_scale, int* status, const int* seed_index, void* stream);
+ * matvecs (tcgen05, one d/128-CTA cluster per two blocks, pool in shared memory; passes 1..iters multiply the
+ * fp16 plane of a, the Rayleigh-quotient pass the full split a).  Blocks whose pool collapses are re-run by
+ * dash_power_iteration's kernel on ema (zero matrix -> lambda 0, reseeded retry); ema may be NULL, leaving
+ * status 3 for them.  Replaces the inner loop of spectral.multi_power_iteration (spectral.py:77-112). */
+int dash_power_iteration_split(const dash_stack* a, const float* ema, float eps, int pool, int iters,
+                               unsigned long long seed, float* scale, float* inv_scale, int* status,
+                               const int* seed_index, void* stream);
 /* Block sharding exchange: copy blocks[b] (device table) of the flat space to/from the block-major
  * packed buffer at offsets pos[b] (device), around the all-gather of updated parameter shards. */
 int dash_pack_blocks(const dash_block* blocks, int n, const long long* pos, const float* flat, float* packed,

@@ -87,8 +87,8 @@ _SIGNATURES: dict[str, tuple] = {
     "dash_fro_scale": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
     "dash_power_iteration": (c_int, [c_void_p, c_int, c_int, c_float, c_int, c_int, c_ull, c_void_p, c_void_p,
                                      c_void_p, c_void_p, c_void_p, c_void_p]),
-    "dash_power_iteration_split": (c_int, [_P, c_int, c_int, c_ull, c_void_p, c_void_p, c_void_p, c_void_p,
-                                           c_void_p]),
+    "dash_power_iteration_split": (c_int, [_P, c_void_p, c_float, c_int, c_int, c_ull, c_void_p, c_void_p,
+                                           c_void_p, c_void_p, c_void_p]),
     "dash_block_seed": (c_ull, [c_ull, c_ull]),
     "dash_pack_blocks": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
     "dash_unpack_blocks": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),

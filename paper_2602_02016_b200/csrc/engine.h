@@ -28,6 +28,9 @@ int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtenso
                 cudaStream_t stream, int* counter, const int* gate = nullptr, double flops = 0.0, int uniform = 0,
                 double issued = 0.0, const GemmWide* wide = nullptr);
 void note_launch(int n = 1);  // count non-GEMM kernel launches
+// fp32 cluster power iteration re-run for the blocks whose status is 3 (collapsed tensor-core pool)
+int pi_retry_launch(const float* ema, int n, int d, float eps, int pool, int iters, unsigned long long seed,
+                    float* scale, float* inv_scale, int* status, const int* seed_index, cudaStream_t st);
 int gemm_kblock();            // K-block of the GEMM launches (64, or 32 under DASH_KB=32)
 extern std::atomic<unsigned long long> g_launches;
 void gemm_timing_enable(int on);

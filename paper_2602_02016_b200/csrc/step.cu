@@ -431,11 +431,14 @@ __global__ void __launch_bounds__(kPi2Threads, 1) pi2_kernel(const float* __rest
                                                              float* __restrict__ scale, float* __restrict__ inv_scale,
                                                              int* __restrict__ status,
                                                              const int* __restrict__ seed_index, int exp_flags,
-                                                             float* __restrict__ vec_out) {
+                                                             float* __restrict__ vec_out, int retry_only) {
   cg::cluster_group cl = cg::this_cluster();
   const int C = static_cast<int>(cl.num_blocks());
   const int q = static_cast<int>(cl.block_rank());
   const int m = blockIdx.x / C;
+  // retry mode: only blocks the tensor-core kernel flagged (status 3, collapsed pool) run; the whole cluster of
+  // every other block leaves before touching distributed shared memory
+  if (retry_only && status[m] != 3) return;
   const int R = ((d + C - 1) / C + 3) / 4 * 4;  // rows per CTA, a multiple of 4 (16-byte aligned slabs)
   const bool vec = d % 4 == 0;
   const int row0 = q * R;
@@ -575,7 +578,7 @@ __global__ void __launch_bounds__(kPi2Threads, 1) pi2_kernel(const float* __rest
 
 static int pi2_launch(const float* ema, int n, int d, float eps, int pool, int iters, unsigned long long seed,
                       float* scale, float* inv_scale, int* status, const int* seed_index, float* vec_out,
-                      cudaStream_t st) {
+                      cudaStream_t st, int retry_only = 0) {
   int C = (d + kPi2R - 1) / kPi2R;
   if (C > 8) return DASH_EINVAL;
   if (C < 1) C = 1;
@@ -599,9 +602,14 @@ static int pi2_launch(const float* ema, int n, int d, float eps, int pool, int i
   cfg.numAttrs = 1;
   static const int exp_flags = getenv("DASH_PI_EXP") ? atoi(getenv("DASH_PI_EXP")) : 0;  // experiment knob
   cudaError_t e = cudaLaunchKernelEx(&cfg, pi2_kernel, ema, d, eps, pool, iters, seed, scale, inv_scale, status,
-                                     seed_index, exp_flags, vec_out);
+                                     seed_index, exp_flags, vec_out, retry_only);
   note_launch();
   return e == cudaSuccess ? DASH_OK : DASH_ECUDA;
+}
+
+int pi_retry_launch(const float* ema, int n, int d, float eps, int pool, int iters, unsigned long long seed,
+                    float* scale, float* inv_scale, int* status, const int* seed_index, cudaStream_t st) {
+  return pi2_launch(ema, n, d, eps, pool, iters, seed, scale, inv_scale, status, seed_index, nullptr, st, 1);
 }
 
 // ---------------------------------------------------------------------------- grafted update

@@ -692,6 +692,8 @@ def save_state(state: ShampooState, cfg: ShampooConfig, path) -> None:
 
     The device state is fp32; every value is written as the float64 of that fp32 number (%.17g), so a
     reference process can load_state it, and our load_state reads reference checkpoints."""
+    if any(r.group < 0 for lay in state.layers for r in lay.left_refs + (lay.right_refs or ())):
+        raise ValueError("save_state needs the full optimizer state; this is one rank's shard of a ShardedDash")
     lines = ["# blockshampoo checkpoint v1", f"step = {state.step}"]
     lines.extend(_config_echo(cfg))
     lines.append(f"momentum = {0 if state.momentum is None else 1}")

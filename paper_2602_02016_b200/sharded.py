@@ -23,7 +23,7 @@ import torch
 from . import _lib
 from .balance import block_balance, block_cost
 from .shampoo import (GroupSpec, LayerState, PrecondGroup, ShampooConfig, ShampooState, SlotRef, _Runtime,
-                      accumulate, block_rows, build_layout, refresh_inverse_roots)
+                      accumulate, block_rows, build_layout, check_step_status, refresh_inverse_roots)
 from .spectral import block_seed
 
 
@@ -92,7 +92,15 @@ def packed_positions(units: list[Unit], idxs: list[int]) -> np.ndarray:
 
 
 class ShardedDash:
-    """DASH optimizer whose preconditioner work is sharded by gradient block across ranks."""
+    """DASH optimizer whose preconditioner work is sharded by gradient block across ranks.
+
+    ``step`` runs this rank's blocks (same kernels and global per-block seeds as the 1-GPU step), agrees on
+    errors with the other ranks (an all-reduce of one flag before the exchange, so a rank that raised in its
+    refresh never leaves the others waiting in the all-gather), packs its updated blocks and all-gathers every
+    rank's shard (NCCL; a gloo group stages the exchange through host memory).  ``state`` is rank-local: its
+    groups hold only the owned blocks, and each layer's slot refs point into them (SlotRef(-1, -1) for blocks
+    another rank owns), so ``save_state`` refuses it rather than writing a partial checkpoint.
+    """
 
     def __init__(self, params, cfg: ShampooConfig, rank: int, world: int, group=None):
         import torch.distributed as dist
@@ -114,7 +122,8 @@ class ShardedDash:
             roots.diagonal(dim1=1, dim2=2).fill_(1.0)
             groups.append(PrecondGroup(sp.dim, sp.exponent, sp.members,
                                        torch.zeros((n, sp.dim, sp.dim), dtype=torch.float32, device=dev), roots))
-        self.state = ShampooState(step=0, layers=layers, groups=groups, adam=[], momentum=None)
+        local_layers = [_local_layer(lay, slot_of) for lay in layers]
+        self.state = ShampooState(step=0, layers=local_layers, groups=groups, adam=[], momentum=None)
         self.state.runtime = _Runtime(self.state, shapes, cfg.block_size, cfg.graft.beta1 > 0.0, owned=owned,
                                       slot_of=slot_of)
         rt = self.state.runtime
@@ -128,8 +137,10 @@ class ShardedDash:
         # exchange layout: rank q's blocks packed block-major (matrix blocks, then chunks) in order
         sizes = [int(packed_positions(self.units, a)[-1]) for a in self.assignment]
         self.max_packed = max(sizes)
+        self.allgather_bytes = 4 * self.max_packed * world
         self.send = torch.zeros(self.max_packed, dtype=torch.float32, device=dev)
         self.recv = torch.zeros(world * self.max_packed, dtype=torch.float32, device=dev)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
         self.tables = []
         for q in range(world):
             ow = {(self.units[i].layer_id, self.units[i].idx) for i in self.assignment[q]}
@@ -140,30 +151,70 @@ class ShardedDash:
                                dtype=torch.int64, device=dev)
             self.tables.append((blocks, pos, len(rows)))
 
+    @property
+    def backend(self) -> str:
+        return self.dist.get_backend(self.group)
+
     # ------------------------------------------------------------------ step
-    def step_local(self, params, grads, seed: int = 0):
+    def step_local(self, params, grads, seed: int = 0, events: dict | None = None):
         """This rank's share of the step: stats, roots and updates of its own blocks (into theta_out)."""
         st, cfg, rt = self.state, self.cfg, self.state.runtime
         t = st.step
+
+        def mark(name):
+            if events is not None:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record()
+                events.setdefault(name, []).append(ev)
+
+        mark("start")
         accumulate(st, grads, cfg)
-        refresh_inverse_roots(st, cfg, seed=block_seed(seed, t))
+        mark("accumulated")
+        refresh_inverse_roots(st, cfg, seed=block_seed(seed, t), defer_check=True)
+        mark("refreshed")
         rt.load(rt.theta, params)
         rt.theta_out.copy_(rt.theta)
         _lib.check(_lib.lib().dash_plan_apply(rt.plan, rt.theta.data_ptr(), rt.theta_out.data_ptr(),
                                               float(cfg.lr.value(t)), _lib.stream_ptr()), "dash_plan_apply")
+        mark("applied")
+        check_step_status(st)
         st.step = t + 1
         return rt.theta_out
+
+    def _all_gather(self) -> None:
+        if self.backend == "nccl":
+            self.dist.all_gather_into_tensor(self.recv, self.send, group=self.group)
+            return
+        host = torch.empty(self.world * self.max_packed, dtype=torch.float32)  # gloo: stage through the host
+        self.dist.all_gather_into_tensor(host, self.send.cpu(), group=self.group)
+        self.recv.copy_(host)
 
     def step(self, params, grads, seed: int = 0, events: dict | None = None):
         """One sharded DASH step; `params` (CUDA tensors) are updated in place on every rank."""
         rt = self.state.runtime
-        self.step_local(params, grads, seed)
+        failure = None
+        try:
+            self.step_local(params, grads, seed, events)
+        except Exception as exc:  # noqa: BLE001 - re-raised after the ranks agree
+            failure = exc
+        self.flag.fill_(1 if failure is not None else 0)
+        if self.backend == "nccl":
+            self.dist.all_reduce(self.flag, op=self.dist.ReduceOp.MAX, group=self.group)
+            bad = int(self.flag.item())
+        else:
+            f = self.flag.cpu()
+            self.dist.all_reduce(f, op=self.dist.ReduceOp.MAX, group=self.group)
+            bad = int(f.item())
+        if failure is not None:
+            raise failure
+        if bad:
+            raise RuntimeError("DASH step failed on another rank (see its error); no parameters were exchanged")
         L = _lib.lib()
         blocks, pos, n = self.tables[self.rank]
         local_pos = pos - self.rank * self.max_packed
         _lib.check(L.dash_pack_blocks(blocks.data_ptr(), n, local_pos.data_ptr(), rt.theta_out.data_ptr(),
                                       self.send.data_ptr(), _lib.stream_ptr()), "dash_pack_blocks")
-        self.dist.all_gather_into_tensor(self.recv, self.send, group=self.group)
+        self._all_gather()
         for q in range(self.world):
             if q == self.rank:
                 continue
@@ -172,7 +223,21 @@ class ShardedDash:
                                             rt.theta_out.data_ptr(), _lib.stream_ptr()), "dash_unpack_blocks")
         for p_, o in zip(params, rt.views(rt.theta_out)):
             p_.copy_(o)
+        if events is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            events.setdefault("exchanged", []).append(ev)
         return params
+
+
+def _local_layer(lay: LayerState, slot_of) -> LayerState:
+    """The layer with its slot refs remapped to the rank-local groups (SlotRef(-1, -1): another rank's block)."""
+    def refs(side, n):
+        return tuple(slot_of.get((lay.layer_id, side, i), SlotRef(-1, -1)) for i in range(n))
+
+    n = len(lay.left_refs)
+    return LayerState(lay.layer_id, lay.shape, lay.layout, lay.chunk_bounds, refs("L", n),
+                      refs("R", n) if lay.right_refs is not None else None)
 
 
 def _all_keys(layers):

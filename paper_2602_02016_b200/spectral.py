@@ -67,7 +67,8 @@ def power_iteration_scales(ema: torch.Tensor, eps: float, pool: int, iters: int,
         raise ValueError(f"the B200 power iteration supports pool <= {MAX_POOL}")
     n, d = ema.shape[0], ema.shape[1]
     if a_split is not None and vec_out is None and d % 128 == 0 and d <= 1024 and not os.environ.get("DASH_PI_FP32"):
-        st = _lib.lib().dash_power_iteration_split(a_split.ref(), int(pool), int(iters), int(seed) & (2**64 - 1),
+        st = _lib.lib().dash_power_iteration_split(a_split.ref(), ema.data_ptr(), float(eps), int(pool), int(iters),
+                                                   int(seed) & (2**64 - 1),
                                                    scale.data_ptr(), inv_scale.data_ptr(), status.data_ptr(),
                                                    seed_index.data_ptr() if seed_index is not None else None,
                                                    _lib.stream_ptr())

@@ -34,7 +34,7 @@ BENCH_SHAPES = [(2048, 2048), (5632, 2048), (2048, 5632), (2048,)]  # 953M-set l
 
 
 def test_bench_config_multi_group_steps_vs_oracle():
-    """bench.py's solver settings on 953M layer shapes: groups 512/p4 (2), 1024/p2 (2), 1024/p4 (36)."""
+    """bench.py's solver settings on 953M layer shapes: groups 512/p4 (4), 1024/p2 (2), 1024/p4 (52)."""
     rng = np.random.default_rng(7)
     params = [rng.standard_normal(s) * 0.02 for s in BENCH_SHAPES]
     grads = [[rng.standard_normal(s) * 1e-3 for s in BENCH_SHAPES] for _ in range(3)]
@@ -42,7 +42,7 @@ def test_bench_config_multi_group_steps_vs_oracle():
         method="ndb", tolerance=0.0, max_iters=10, precision=PrecisionMode.EMULATED32))
     ocfg = core.OracleConfig(block_size=1024, method="ndb", tolerance=0.0, max_iters=10)
     st, ost = shampoo.init_state(params, cfg), core.init_state(params, ocfg)
-    assert [(g.dim, g.exponent, len(g.members)) for g in st.groups] == [(512, 4, 2), (1024, 2, 2), (1024, 4, 36)]
+    assert [(g.dim, g.exponent, len(g.members)) for g in st.groups] == [(512, 4, 4), (1024, 2, 2), (1024, 4, 52)]
     cur, ocur = params, params
     for gs in grads:
         prev, oprev = cur, ocur

@@ -195,24 +195,30 @@ def test_c1_config_fixed_iterations_vs_oracle():
 
 @pytest.mark.parametrize("d", [128, 256, 1024])
 def test_power_iteration_tensor_cores_vs_oracle(d):
-    """Tensor-core PI (split stack of a = ema + eps I, d % 128 == 0) against the float64 oracle restatement
-    with the same per-block seeds (spectral.py:87-117): lambda within 2e-6 relative."""
-    conds = [(10.0, 0.5), (1e3, 2.0), (50.0, 1e-3)]
-    ema = np.stack([core.random_spd(d, c, seed=i, scale=s) for i, (c, s) in enumerate(conds)])
+    """Tensor-core PI (split stack of a = ema + eps I, d % 128 == 0; two blocks per cluster, an odd count leaves
+    one slot empty) against the float64 oracle restatement with the same per-block seeds (spectral.py:87-117).
+    Passes 1..30 multiply the fp16 plane of a, the quotient pass the full split a: lambda within 2e-5 relative.
+    A zero block collapses the pool and is re-run by the fp32 kernel: lambda 0, status 1 (non-positive scale)."""
+    conds = [(10.0, 0.5), (1e3, 2.0), (50.0, 1e-3), (1e2, 1.0)]
+    ema = np.stack([core.random_spd(d, c, seed=i, scale=s) for i, (c, s) in enumerate(conds)] + [np.zeros((d, d))])
     eps, seed = 1e-10, 777
     et = torch.as_tensor(ema, dtype=torch.float32, device="cuda")
-    a_split = linalg.SplitStack.from_float(et + eps * torch.eye(d, device="cuda"))
+    a_split = linalg.SplitStack.from_float(et + eps * torch.eye(d, device="cuda") * torch.tensor(
+        [1.0] * 4 + [0.0], device="cuda")[:, None, None])
     n = ema.shape[0]
     sc, inv = torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda")
     st = torch.zeros(n, dtype=torch.int32, device="cuda")
-    spectral.power_iteration_scales(et, eps, 16, 30, seed, sc, inv, st, a_split=a_split)
-    sc2, inv2 = torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda")
-    spectral.power_iteration_scales(et, eps, 16, 30, seed, sc2, inv2, st)  # fp32 kernel on ema
+    spectral.power_iteration_scales(et[:4], eps, 16, 30, seed, sc[:4], inv[:4], st[:4], a_split=a_split.head(4))
     want = [2.0 * core.multi_power_iteration(ema[i] + eps * np.eye(d), 16, 30, core.block_seed(seed, i))
-            for i in range(n)]
-    np.testing.assert_allclose(sc.cpu().numpy(), want, rtol=2e-6)
-    np.testing.assert_allclose(sc.cpu().numpy(), sc2.cpu().numpy(), rtol=2e-6)
-    assert int(st.abs().sum()) == 0
+            for i in range(4)]
+    np.testing.assert_allclose(sc[:4].cpu().numpy(), want, rtol=2e-5)
+    assert int(st[:4].abs().sum()) == 0
+    # the zero block (eps = 0): collapsed pool -> retry kernel -> lambda 0 (spectral.py:99-101)
+    sc5, inv5 = torch.zeros(5, device="cuda"), torch.zeros(5, device="cuda")
+    st5 = torch.zeros(5, dtype=torch.int32, device="cuda")
+    spectral.power_iteration_scales(et, 0.0, 16, 30, seed, sc5, inv5, st5, a_split=a_split)
+    assert float(sc5[4]) == 0.0 and int(st5[4]) == 1
+    np.testing.assert_allclose(sc5[:4].cpu().numpy(), want, rtol=2e-5)
 
 
 @pytest.mark.parametrize("b", [640, 1024])

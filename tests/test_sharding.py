@@ -150,3 +150,100 @@ def test_two_shards_equal_unsharded_step_bitwise():
             ix = torch.tensor(_flat_index(layers, offsets, units[i]), device="cuda")
             merged[ix] = outs[r][ix]
     assert torch.equal(merged, ref_flat)
+
+
+def _sharded_worker(rank, world, port, q):
+    """One rank of a world-2 ShardedDash: the full step (accumulate, refresh, apply, C-ABI pack, all-gather,
+    unpack) on cuda:0 over gloo (host-staged exchange), three steps, then the flat parameters go back."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2602_02016_b200.shampoo import ShampooConfig, SolverConfig
+    from paper_2602_02016_b200.sharded import ShardedDash
+
+    rng = np.random.default_rng(0)
+    shapes = [(96, 64), (64,), (40, 72), (130, 33)]
+    params = [torch.tensor(rng.standard_normal(s), dtype=torch.float32, device="cuda") for s in shapes]
+    grads = [[torch.tensor(rng.standard_normal(s), dtype=torch.float32, device="cuda") for s in shapes]
+             for _ in range(3)]
+    cfg = ShampooConfig(block_size=32, solver=SolverConfig(tolerance=0.0, max_iters=10))
+    opt = ShardedDash(params, cfg, rank=rank, world=world)
+    events = {}
+    for gs in grads:
+        opt.step(params, gs, seed=5, events=events)
+    torch.cuda.synchronize()
+    q.put((rank, torch.cat([p.reshape(-1) for p in params]).cpu().numpy(), len(events.get("exchanged", []))))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_sharded_step_world2_equals_single_gpu_bitwise():
+    """ShardedDash.step end to end on 2 ranks == the 1-GPU step, bit for bit, on both ranks."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2602_02016_b200.shampoo import ShampooConfig, SolverConfig, init_state, step
+
+    rng = np.random.default_rng(0)
+    shapes = [(96, 64), (64,), (40, 72), (130, 33)]
+    params = [torch.tensor(rng.standard_normal(s), dtype=torch.float32, device="cuda") for s in shapes]
+    grads = [[torch.tensor(rng.standard_normal(s), dtype=torch.float32, device="cuda") for s in shapes]
+             for _ in range(3)]
+    cfg = ShampooConfig(block_size=32, solver=SolverConfig(tolerance=0.0, max_iters=10))
+    st = init_state(params, cfg)
+    cur = [p.clone() for p in params]
+    for gs in grads:
+        cur, st = step(st, cur, gs, cfg, seed=5)
+    want = torch.cat([c.reshape(-1) for c in cur]).cpu().numpy()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {r: (flat, nex) for r, flat, nex in (q.get(timeout=300) for _ in procs)}
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(2):
+        assert res[r][1] == 3
+        np.testing.assert_array_equal(res[r][0], want)
+
+
+def _failing_worker(rank, world, port, q):
+    """Rank 1 raises inside its refresh (a tolerance its precision cannot reach); rank 0 must not hang."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2602_02016_b200.linalg import PrecisionMode
+    from paper_2602_02016_b200.shampoo import ShampooConfig, SolverConfig
+    from paper_2602_02016_b200.sharded import ShardedDash
+
+    rng = np.random.default_rng(1)
+    shapes = [(64, 64), (64, 64)]
+    params = [torch.tensor(rng.standard_normal(s), dtype=torch.float32, device="cuda") for s in shapes]
+    grads = [torch.tensor(rng.standard_normal(s), dtype=torch.float32, device="cuda") for s in shapes]
+    tol = 1e-12 if rank == 1 else 0.0
+    cfg = ShampooConfig(block_size=32, solver=SolverConfig(method="cn", tolerance=tol, max_iters=4,
+                                                           precision=PrecisionMode.EMULATED32))
+    opt = ShardedDash(params, cfg, rank=rank, world=world)
+    try:
+        opt.step(params, grads)
+        q.put((rank, "ok"))
+    except Exception as exc:  # noqa: BLE001
+        q.put((rank, type(exc).__name__))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_sharded_step_error_reaches_every_rank():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_failing_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: "RuntimeError", 1: "ConvergenceError"}
