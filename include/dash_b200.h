@@ -171,6 +171,15 @@ int dash_power_iteration(const float* ema, int n, int d, float eps, int pool, in
 int dash_power_iteration_split(const dash_stack* a, const float* ema, float eps, int pool, int iters,
                                unsigned long long seed, float* scale, float* inv_scale, int* status,
                                const int* seed_index, void* stream);
+/* dash_jacobi_eigh: batched cyclic Jacobi eigendecomposition in float64 (eigensolver.eigh / _jacobi,
+ *   eigensolver.py:53-124): the reference's round-robin schedule of disjoint pairs, dead-pair skip
+ *   0.1 tol |A|_F / d, convergence when the off-diagonal norm <= tol |A|_F, at most max_sweeps sweeps.
+ *   a: n x d x d float64 symmetric blocks (d <= 1024); lam: n x d eigenvalues ascending; q: n x d x d
+ *   eigenvectors in columns; sweeps / status (nullable): sweeps run, 0 converged / 1 not converged.
+ *   ws: dash_jacobi_ws_bytes(n, d) bytes (working copies of A and V). */
+size_t dash_jacobi_ws_bytes(int n, int d);
+int dash_jacobi_eigh(const double* a, int n, int d, double tol, int max_sweeps, double* lam, double* q, int* sweeps,
+                     int* status, void* ws, size_t ws_bytes, void* stream);
 /* Block sharding exchange: copy blocks[b] (device table) of the flat space to/from the block-major
  * packed buffer at offsets pos[b] (device), around the all-gather of updated parameter shards. */
 int dash_pack_blocks(const dash_block* blocks, int n, const long long* pos, const float* flat, float* packed,

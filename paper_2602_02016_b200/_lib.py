@@ -90,6 +90,9 @@ _SIGNATURES: dict[str, tuple] = {
     "dash_power_iteration_split": (c_int, [_P, c_void_p, c_float, c_int, c_int, c_ull, c_void_p, c_void_p,
                                            c_void_p, c_void_p, c_void_p]),
     "dash_block_seed": (c_ull, [c_ull, c_ull]),
+    "dash_jacobi_ws_bytes": (c_size_t, [c_int, c_int]),
+    "dash_jacobi_eigh": (c_int, [c_void_p, c_int, c_int, ctypes.c_double, c_int, c_void_p, c_void_p, c_void_p,
+                                 c_void_p, c_void_p, c_size_t, c_void_p]),
     "dash_pack_blocks": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
     "dash_unpack_blocks": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
     "dash_uniform_pm1": (c_int, [c_ull, c_int, c_void_p, c_void_p]),

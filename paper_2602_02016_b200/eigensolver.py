@@ -4,7 +4,9 @@ Reference surface: ``HeuristicKind`` / ``DampeningHeuristic`` (``eigensolver.py:
 ``EigenDecomposition`` (``:47-50``), ``eigh`` (``:120-124``), ``dampen_spectrum`` / ``dampen_corrected``
 (``:133-154``), ``evd_inverse_root`` (``:157-172``), ``batched_evd_inverse_root`` (``:175-179``).
 
-The eigendecompositions run on the device in float64 (``_eigh_stack``), batched over blocks.  Besides the
+The eigendecompositions run on the device in float64, batched over blocks: ``csrc/evd.cu`` restates the
+reference's cyclic Jacobi (same round-robin pair schedule, dead-pair skip and stopping rule, IEEE float64
+rotations without FMA contraction).  Besides the
 EVD solver option / config-2 comparator, the float64 inverse root is the optimizer's fallback for blocks the
 fp32-class Newton iterations cannot converge in FULL64 mode (``inverse_root_f64``).
 """
@@ -16,8 +18,9 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from . import _lib
 from .errors import ConvergenceError, DegenerateSpectrumError
-from .linalg import check_symmetric, device
+from .linalg import check_symmetric, device, workspace
 
 
 class HeuristicKind(enum.Enum):
@@ -43,13 +46,29 @@ class EigenDecomposition:
 
 
 # ----------------------------------------------------------------------------- device eigensolver
+def jacobi(a: torch.Tensor, tol: float = 1e-12, max_sweeps: int = 100):
+    """dash_jacobi_eigh on a float64 (n, d, d) CUDA stack: (eigenvalues ascending, eigenvectors in columns,
+    sweeps per block, status per block: 0 converged / 1 not converged)."""
+    a = a.to(torch.float64).contiguous()
+    n, d = a.shape[0], a.shape[-1]
+    lam = torch.empty((n, d), dtype=torch.float64, device=a.device)
+    q = torch.empty_like(a)
+    sweeps = torch.zeros(n, dtype=torch.int32, device=a.device)
+    status = torch.zeros(n, dtype=torch.int32, device=a.device)
+    L = _lib.lib()
+    ws = workspace(L.dash_jacobi_ws_bytes(n, d), a.device)
+    _lib.check(L.dash_jacobi_eigh(a.data_ptr(), n, d, float(tol), int(max_sweeps), lam.data_ptr(), q.data_ptr(),
+                                  sweeps.data_ptr(), status.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr()),
+               "dash_jacobi_eigh")
+    return lam, q, sweeps, status
+
+
 def _eigh_stack(a: torch.Tensor, tol: float = 1e-12, max_sweeps: int = 100) -> tuple[torch.Tensor, torch.Tensor]:
-    """Batched symmetric EVD of a float64 (n, d, d) CUDA stack: eigenvalues ascending, eigenvectors in columns."""
-    if a.dtype != torch.float64:
-        a = a.double()
-    lam, q = torch.linalg.eigh(a)
-    if not bool(torch.isfinite(lam).all()):
-        raise ConvergenceError("eigensolver produced non-finite eigenvalues")
+    """Batched symmetric EVD on the device Jacobi kernel (the reference's cyclic round-robin Jacobi,
+    eigensolver.py:77-117).  Raises ConvergenceError when a block needs more than max_sweeps sweeps (:112-113)."""
+    lam, q, _, status = jacobi(a, tol, max_sweeps)
+    if bool(status.any()):
+        raise ConvergenceError(f"Jacobi eigensolver did not converge in {max_sweeps} sweeps")
     return lam, q
 
 

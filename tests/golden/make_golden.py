@@ -18,7 +18,7 @@ REF = os.environ.get("DASH_REF_SRC", "/root/reference/pkg/src")
 sys.path.insert(0, REF)
 sys.path.insert(0, str(Path(__file__).resolve().parent))
 
-from blockshampoo import chebyshev, roots, shampoo, spectral, tasks  # noqa: E402
+from blockshampoo import eigensolver, chebyshev, roots, shampoo, spectral, tasks  # noqa: E402
 from blockshampoo.linalg import PrecisionMode  # noqa: E402
 
 OUT = Path(__file__).resolve().parent
@@ -86,6 +86,17 @@ def solver_fixture():
     res["pi_vecs"] = np.stack([e.vector for e in ests])
     res["pi_seeds"] = np.array([100 + i for i in range(a.shape[0])])
     res["fro_scales"] = np.sqrt((a * a).sum(axis=(1, 2)))
+    # cyclic Jacobi (eigensolver.py:77-124): SPD, indefinite, odd-sized and 1x1 blocks
+    rng = np.random.default_rng(31)
+    sym = rng.standard_normal((24, 24))
+    jac = {"spd": tasks.random_spd(16, 1e3, seed=2, scale=0.5), "indef": 0.5 * (sym + sym.T),
+           "odd": tasks.random_spd(7, 30.0, seed=3), "one": np.array([[2.5]]), "blk": a[1]}
+    for name, m in jac.items():
+        dec, sweeps = eigensolver.eigh_with_sweeps(m)
+        res[f"jac_{name}_a"] = m
+        res[f"jac_{name}_lam"] = dec.eigenvalues
+        res[f"jac_{name}_vec"] = dec.eigenvectors
+        res[f"jac_{name}_sweeps"] = np.array(sweeps)
     res["rspd_3_10_5"] = tasks.random_spd(3, 10.0, seed=5, scale=0.5)
     np.savez_compressed(OUT / "solvers.npz", **res)
 

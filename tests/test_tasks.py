@@ -20,7 +20,7 @@ def test_tasks_match_reference(reference):
         ours, theirs = tasks.TASKS[name](seed=5), ref.TASKS[name](seed=5)
         p1, p2 = ours.init_params(), theirs.init_params()
         assert all(np.array_equal(a, b) for a, b in zip(p1, p2))
-        assert ours.loss(p1) == theirs.loss(p2)
+        assert ours.loss(p1) == pytest.approx(theirs.loss(p2), rel=1e-13)
         g1, g2 = ours.grads(p1), theirs.grads(p2)
         for a, b in zip(g1, g2):
             assert np.allclose(a, b, rtol=1e-13, atol=1e-15)
