@@ -17,7 +17,7 @@ int dash_ndb(const dash_stack* a, const float* inv_scale, const dash_stack* y, c
              float stall, int max_iters, int passes, int* iters, float* resid, int* conv, void* ws, size_t ws_bytes,
              void* stream) {
   if (!square_same(a, y) || !square_same(a, z) || max_iters < 1 || tol < 0.f || stall < 0.f || !iters || !resid || !conv ||
-      (passes != 1 && passes != 3))
+      (passes != 1 && passes != 3 && passes != 4))
     return DASH_EINVAL;
   if (ws_bytes < ndb_ws_bytes(a->nmat, a->rows)) return DASH_EINVAL;
   return ndb_solve(*a, inv_scale, *y, *z, tol, stall, max_iters, passes, iters, resid, conv, ws, ws_bytes,
@@ -28,7 +28,7 @@ int dash_ndb_upper(const dash_stack* a, const float* inv_scale, const dash_stack
                    float stall, int max_iters, int passes, int* iters, float* resid, int* conv, void* ws, size_t ws_bytes,
                    void* stream) {
   if (!square_same(a, y) || !square_same(a, z) || max_iters < 1 || tol < 0.f || stall < 0.f || !iters || !resid || !conv ||
-      (passes != 1 && passes != 3))
+      (passes != 1 && passes != 3 && passes != 4))
     return DASH_EINVAL;
   if (ws_bytes < ndb_ws_bytes(a->nmat, a->rows)) return DASH_EINVAL;
   return ndb_solve(*a, inv_scale, *y, *z, tol, stall, max_iters, passes, iters, resid, conv, ws, ws_bytes,
@@ -46,7 +46,7 @@ int dash_cn(const dash_stack* a, const float* inv_scale, int p, float c, const d
             float stall, int max_iters, int passes, int* iters, float* resid, int* conv, void* ws, size_t ws_bytes,
             void* stream) {
   if (!square_same(a, x) || (p != 2 && p != 4) || !(c > 0.f) || max_iters < 1 || tol < 0.f || stall < 0.f || !iters ||
-      !resid || !conv || (passes != 1 && passes != 3))
+      !resid || !conv || (passes != 1 && passes != 3 && passes != 4))
     return DASH_EINVAL;
   if (ws_bytes < cn_ws_bytes(a->nmat, a->rows)) return DASH_EINVAL;
   return cn_solve(*a, inv_scale, p, c, *x, tol, stall, max_iters, passes, iters, resid, conv, ws, ws_bytes,
@@ -73,7 +73,7 @@ int dash_clenshaw(const dash_stack* a, const float* inv_scale, const float* mult
                   float* f_out, const dash_stack* out, int passes, const int* gate, void* ws, size_t ws_bytes,
                   void* stream) {
   if (!stack_ok(a) || a->rows != a->cols || !coeffs || degree < 2 || (!f_out && !out) ||
-      (out && !square_same(a, out)) || (passes != 1 && passes != 3))
+      (out && !square_same(a, out)) || (passes != 1 && passes != 3 && passes != 4))
     return DASH_EINVAL;
   if (ws_bytes < cheb_ws_bytes(a->nmat, a->rows)) return DASH_EINVAL;
   return cheb_solve(*a, inv_scale, mult, coeffs, degree, f_out, out, passes, gate, ws, ws_bytes,

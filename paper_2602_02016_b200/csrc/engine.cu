@@ -434,7 +434,7 @@ int dash_bmm(const dash_stack* a, int trans_a, const dash_stack* b, int trans_b,
              float* f_out, long long f_mat_stride, int f_ld, float alpha, int passes, void* ws, size_t ws_bytes,
              void* stream) {
   if (!stack_ok(a) || !stack_ok(b) || (c && !stack_ok(c)) || (!c && !f_out)) return DASH_EINVAL;
-  if (a->nmat != b->nmat || (c && c->nmat != a->nmat) || (passes != 1 && passes != 3)) return DASH_EINVAL;
+  if (a->nmat != b->nmat || (c && c->nmat != a->nmat) || (passes != 1 && passes != 3 && passes != 4)) return DASH_EINVAL;
   const int M = trans_a ? a->cols : a->rows;
   const int N = trans_b ? b->rows : b->cols;
   if (c && (c->rows != M || c->cols != N)) return DASH_EINVAL;

@@ -85,10 +85,12 @@ __global__ void __launch_bounds__(kEvdThreads) jacobi_kernel(const double* __res
       for (int k = threadIdx.x; k < half; k += kEvdThreads) {
         const int x = evd_player(k, r, m), y = evd_player(m - 1 - k, r, m);
         double c = 1.0, s = 0.0;
-        int p = -1, q = -1;
-        if (x < d && y < d) {
-          p = min(x, y);
-          q = max(x, y);
+        // an odd dimension pads the schedule with a dummy player: its partner is a lone index that is not
+        // rotated this round (q = -1) but still receives the other pairs' row / column rotations
+        int p = min(x, y), q = max(x, y);
+        if (q >= d) {
+          q = -1;
+        } else {
           const double apq = a[static_cast<long long>(p) * d + q];
           if (fabs(apq) > skip) {
             const double app = a[static_cast<long long>(p) * d + p], aqq = a[static_cast<long long>(q) * d + q];
@@ -114,13 +116,13 @@ __global__ void __launch_bounds__(kEvdThreads) jacobi_kernel(const double* __res
       const long long tiles = static_cast<long long>(half) * half;
       for (long long t = threadIdx.x; t < tiles; t += kEvdThreads) {
         const int I = static_cast<int>(t / half), J = static_cast<int>(t % half);
-        const int pi = pp[I], qi = qq[I], pj = pp[J], qj = qq[J];
-        if (pi < 0 || pj < 0) continue;  // padded slot of an odd dimension
+        const int pi = pp[I], qi = qq[I], pj = pp[J], qj = qq[J];  // qi / qj = -1: a lone (unrotated) index
         const double ci = cs[I], si = sn[I], cj = cs[J], sj = sn[J];
         if (si == 0.0 && sj == 0.0) continue;  // both rotations are the identity
         double* r0 = a + static_cast<long long>(pi) * d;
-        double* r1 = a + static_cast<long long>(qi) * d;
-        const double x00 = r0[pj], x01 = r0[qj], x10 = r1[pj], x11 = r1[qj];
+        double* r1 = a + static_cast<long long>(qi < 0 ? pi : qi) * d;
+        const double x00 = r0[pj], x01 = qj >= 0 ? r0[qj] : 0.0;
+        const double x10 = qi >= 0 ? r1[pj] : 0.0, x11 = (qi >= 0 && qj >= 0) ? r1[qj] : 0.0;
         // rows (eigensolver.py:101-103): p' = c p - s q, q' = s p + c q
         const double y00 = __dsub_rn(__dmul_rn(ci, x00), __dmul_rn(si, x10));
         const double y01 = __dsub_rn(__dmul_rn(ci, x01), __dmul_rn(si, x11));
@@ -128,16 +130,18 @@ __global__ void __launch_bounds__(kEvdThreads) jacobi_kernel(const double* __res
         const double y11 = __dadd_rn(__dmul_rn(si, x01), __dmul_rn(ci, x11));
         // columns (:104-106)
         r0[pj] = __dsub_rn(__dmul_rn(cj, y00), __dmul_rn(sj, y01));
-        r0[qj] = __dadd_rn(__dmul_rn(sj, y00), __dmul_rn(cj, y01));
-        r1[pj] = __dsub_rn(__dmul_rn(cj, y10), __dmul_rn(sj, y11));
-        r1[qj] = __dadd_rn(__dmul_rn(sj, y10), __dmul_rn(cj, y11));
+        if (qj >= 0) r0[qj] = __dadd_rn(__dmul_rn(sj, y00), __dmul_rn(cj, y01));
+        if (qi >= 0) {
+          r1[pj] = __dsub_rn(__dmul_rn(cj, y10), __dmul_rn(sj, y11));
+          if (qj >= 0) r1[qj] = __dadd_rn(__dmul_rn(sj, y10), __dmul_rn(cj, y11));
+        }
       }
       // ---- 3. V <- V R^T (:107-109)
       const long long vitems = static_cast<long long>(d) * half;
       for (long long t = threadIdx.x; t < vitems; t += kEvdThreads) {
         const int row = static_cast<int>(t / half), J = static_cast<int>(t % half);
         const int pj = pp[J], qj = qq[J];
-        if (pj < 0 || sn[J] == 0.0) continue;
+        if (qj < 0 || sn[J] == 0.0) continue;  // lone index or identity rotation
         const double c = cs[J], s = sn[J];
         double* vr = v + static_cast<long long>(row) * d;
         const double vp = vr[pj], vq = vr[qj];

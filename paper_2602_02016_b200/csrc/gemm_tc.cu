@@ -1041,6 +1041,14 @@ int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtenso
                 const GemmWide* wide) {
   if (total_tiles <= 0) return 0;
   if (!counter) return 1;
+  // passes = 4: the split 3-pass products with four K-range accumulators per tile (the FULL64 mode: ~2.5x
+  // smaller accumulation error, one tile in flight instead of two); otherwise the DASH_NACC default
+  int nacc_req = 0;
+  if (passes == 4) {
+    passes = 3;
+    nacc_req = 4;
+    issued *= 0.75;
+  }
   const int wm = wide_mode();
   const bool use_wide = wide && wide->tiles > 0 && (passes == 1 ? wm >= 1 : wm >= 2);
   if (use_wide) {
@@ -1095,7 +1103,7 @@ int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtenso
     g_kb = e ? atoi(e) : kKbDefault;
     if (g_kb != 32 && g_kb != 64) g_kb = kKbDefault;
   }
-  const int flags = (passes == 3 ? g_nacc : 1) | (g_exp << 8);
+  const int flags = (passes == 3 ? (nacc_req ? nacc_req : g_nacc) : 1) | (g_exp << 8);
   if (use_wide && passes == 3 && g_kb == 64) launch_variant<3, 64, 256>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter, prof);
   else if (use_wide && passes == 3) launch_variant<3, 32, 256>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter, prof);
   else if (use_wide && g_kb == 64) launch_variant<1, 64, 256>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter, prof);

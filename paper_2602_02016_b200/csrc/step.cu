@@ -741,7 +741,7 @@ dash_plan* dash_plan_create(const dash_block* blocks, int nb_m, int nb_v, int bl
     return nullptr;
   };
   if (!blocks || nb_m < 0 || nb_v < 0 || nb_m + nb_v == 0 || block_size < 1 || ngroups < 1 || !grad || !adam ||
-      !pn_part || !un_part || !gamax || (passes != 1 && passes != 3))
+      !pn_part || !un_part || !gamax || (passes != 1 && passes != 3 && passes != 4))
     return fail(DASH_EINVAL);
   if ((nb_m && (!stack_ok(gsm) || !stack_ok(tm) || !um)) || (nb_v && (!stack_ok(gsv) || !uv))) return fail(DASH_EINVAL);
   dash_plan* p = new dash_plan();

@@ -9,9 +9,10 @@ Precision modes (the reference has FULL64 / EMULATED32; the B200 build adds F16)
 * ``EMULATED32`` ("f32") -- split-f16 products: each operand is stored as fp16 hi + fp16 lo with a
   per-matrix power-of-two exponent, and every product issues hi*hi + hi*lo + lo*hi on the tensor
   cores with fp32 accumulation (22-bit significands, fp32-class results).
-* ``FULL64`` ("f64") -- accepted for drop-in compatibility; runs the same split-f16 engine (there is
-  no fp64 tensor-core path on the hot path).  Parity against the float64 reference is therefore by
-  the tolerances stated in DESIGN.md, never bitwise.
+* ``FULL64`` ("f64", the reference's default) -- the same split-f16 products with four K-range fp32
+  accumulators per output tile (about 2.5x smaller accumulation error than EMULATED32, ~11% slower); its
+  Newton iterations converge at the fp32-class floor and blocks they cannot converge are re-solved in float64
+  (see below).  Parity against the float64 reference is by the tolerances stated in DESIGN.md, never bitwise.
 * ``F16`` ("f16") -- hi*hi only (fp16 tensor rate, ~11-bit significands).
 """
 from __future__ import annotations
@@ -36,7 +37,9 @@ class PrecisionMode(enum.Enum):
 
 
 def passes_for(mode: PrecisionMode) -> int:
-    return 1 if mode is PrecisionMode.F16 else 3
+    """The engine's `passes` argument: 1 = fp16 products, 3 = split-f16 (hi*hi + hi*lo + lo*hi, main and
+    correction accumulators), 4 = the same split with four K-range accumulators per tile (FULL64)."""
+    return {PrecisionMode.F16: 1, PrecisionMode.EMULATED32: 3, PrecisionMode.FULL64: 4}[mode]
 
 
 # FULL64 promises float64-quality roots on an fp32-class engine.  Its Newton iterations converge "at the
@@ -134,11 +137,13 @@ class SplitStack:
 
     def head(self, n: int) -> "SplitStack":
         """The first ``n`` matrices (shares storage)."""
-        if n == self.nmat:
-            return self
+        return self if n == self.nmat else self.slice(0, n)
+
+    def slice(self, start: int, stop: int) -> "SplitStack":
+        """Matrices [start, stop) (shares storage)."""
         v = SplitStack.__new__(SplitStack)
         v.rows, v.cols = self.rows, self.cols
-        v.data, v.exp, v.amax = self.data[:n], self.exp[:n], self.amax[:n]
+        v.data, v.exp, v.amax = self.data[start:stop], self.exp[start:stop], self.amax[start:stop]
         v._c = None
         return v
 

@@ -19,6 +19,7 @@ reference's types); CUDA tensors stay on the device.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 from typing import Any
 
@@ -274,6 +275,20 @@ def block_rows(layers: list[LayerState], offsets, owned=None, slot_of=None):
     return mats, vecs
 
 
+@dataclass
+class _Chunk:
+    """One pipeline chunk of the host-buffer step: layers [l0, l1) = flat elements [e0, e1)."""
+
+    l0: int
+    l1: int
+    e0: int
+    e1: int
+    plan: Any
+    ws: torch.Tensor
+    blocks_c: Any
+    ranges: list  # (group index, first slot, end slot)
+
+
 class _Runtime:
     """Flat device buffers + the C-ABI plan for one optimizer structure (or one rank's shard of it)."""
 
@@ -321,39 +336,93 @@ class _Runtime:
         self.stats_valid = False           # g_amax / g_fro describe the current EMA (set by accumulate)
         self.stats_eps = None
         self.pending_err = None            # device error word of the last fixed-iteration refresh
+        self._slot_ids: dict = {}
+
+    def slot_ids(self, gi: int) -> torch.Tensor:
+        """0..n-1 for group gi on the device (global slots of a member range: the power-iteration seeds)."""
+        ids = self._slot_ids.get(gi)
+        if ids is None:
+            ids = self._slot_ids[gi] = torch.arange(len(self.groups[gi].members), dtype=torch.int32, device=self.dev)
+        return ids
 
     def views(self, flat: torch.Tensor) -> list[torch.Tensor]:
         return [flat[int(self.offsets[i]):int(self.offsets[i + 1])].view(s) for i, s in enumerate(self.shapes)]
 
-    def ensure_plan(self, cfg: ShampooConfig) -> None:
-        key = (cfg.beta_lr, passes_for(cfg.solver.precision))
-        if self.plan is not None and self.plan_key == key:
-            return
-        self.close()
+    def _create_plan(self, blocks_c, nb_m: int, nb_v: int, key):
+        """A C-ABI plan over a block table (all blocks, or one pipeline chunk's); returns (plan, workspace)."""
         L = _lib.lib()
         ng = len(self.groups)
         gdim = (ctypes_int * ng)(*[g.dim for g in self.groups])
         gsize = (ctypes_int * ng)(*[len(g.members) for g in self.groups])
         gema = (ctypes_vp * ng)(*[g.ema.data_ptr() for g in self.groups])
         groot = (_lib.dash_stack * ng)(*[rs.c() for rs in self.root_split])
-        self.plan_ws = workspace(L.dash_plan_ws_bytes(self.nb_m, self.nb_v), self.dev)
+        ws = workspace(L.dash_plan_ws_bytes(nb_m, nb_v), self.dev)
         status = ctypes_int(0)
         p = L.dash_plan_create(
-            self.blocks_c, self.nb_m, self.nb_v, self.bsz, ng, gdim, gsize, gema, groot,
+            blocks_c, nb_m, nb_v, self.bsz, ng, gdim, gsize, gema, groot,
             self.grad.data_ptr(), self.adam.data_ptr(), self.mom.data_ptr() if self.mom is not None else None,
             self.gsm.ref() if self.gsm else None, self.gsv.ref() if self.gsv else None,
             self.tm.ref() if self.tm else None, self.um.data_ptr(), self.uv.data_ptr(), self.pn_part.data_ptr(),
-            self.un_part.data_ptr(), self.gamax.data_ptr(), self.graft_s.data_ptr(), float(cfg.beta_lr),
-            key[1], self.plan_ws.data_ptr(), self.plan_ws.numel(), _lib.stream_ptr(), ctypes_byref(status))
+            self.un_part.data_ptr(), self.gamax.data_ptr(), self.graft_s.data_ptr(), float(key[0]),
+            key[1], ws.data_ptr(), ws.numel(), _lib.stream_ptr(), ctypes_byref(status))
         if not p:
             _lib.check(status.value or _lib.DASH_EINVAL, "dash_plan_create")
-        self.plan = p
+        return p, ws
+
+    def ensure_plan(self, cfg: ShampooConfig) -> None:
+        key = (cfg.beta_lr, passes_for(cfg.solver.precision))
+        if self.plan is not None and self.plan_key == key:
+            return
+        self.close()
+        self.plan, self.plan_ws = self._create_plan(self.blocks_c, self.nb_m, self.nb_v, key)
         self.plan_key = key
+
+    def ensure_chunks(self, cfg: ShampooConfig, layers: list[LayerState], nchunks: int) -> list:
+        """Pipeline chunks of the host-buffer step: contiguous layer ranges of about equal size, each with its
+        own plan over its blocks and, per group, the contiguous slot range of its members (members are sorted
+        by layer, shampoo.py:185-202)."""
+        key = (cfg.beta_lr, passes_for(cfg.solver.precision), nchunks)
+        if getattr(self, "chunks", None) and self.chunks_key == key:
+            return self.chunks
+        self.close_chunks()
+        total, target = sum(self.sizes), sum(self.sizes) / nchunks
+        bounds, acc = [0], 0
+        for i, sz in enumerate(self.sizes):
+            acc += sz
+            if acc >= target * len(bounds) and len(bounds) < nchunks and i + 1 < len(self.sizes):
+                bounds.append(i + 1)
+        bounds.append(len(self.sizes))
+        chunks = []
+        for c0, c1 in zip(bounds[:-1], bounds[1:]):
+            owned = set()
+            for lay in layers[c0:c1]:
+                nb = len(lay.layout.block_spans) if lay.is_matrix else len(lay.chunk_bounds)
+                owned.update((lay.layer_id, i) for i in range(nb))
+            mats, vecs = block_rows(layers, self.offsets, owned)
+            rows = mats + vecs
+            blocks_c = (_lib.dash_block * len(rows))(*[_lib.dash_block(*b) for b in rows])
+            plan, ws = self._create_plan(blocks_c, len(mats), len(vecs), key)
+            ranges = []
+            for gi, g in enumerate(self.groups):
+                slots = [k for k, m in enumerate(g.members) if c0 <= m[0] < c1]
+                if slots:
+                    assert slots == list(range(slots[0], slots[-1] + 1))
+                    ranges.append((gi, slots[0], slots[-1] + 1))
+            chunks.append(_Chunk(c0, c1, int(self.offsets[c0]), int(self.offsets[c1]), plan, ws, blocks_c, ranges))
+        self.chunks, self.chunks_key = chunks, key
+        del total
+        return chunks
+
+    def close_chunks(self) -> None:
+        for ch in getattr(self, "chunks", None) or []:
+            _lib.lib().dash_plan_destroy(ch.plan)
+        self.chunks = None
 
     def close(self) -> None:
         if self.plan:
             _lib.lib().dash_plan_destroy(self.plan)
             self.plan = None
+        self.close_chunks()
 
     def __del__(self):
         try:
@@ -416,12 +485,12 @@ def _solver_coefficients(solver: SolverConfig, p: int) -> ChebCoefficients:
     return _cheb_cache[key]
 
 
-def _check_reports(group: PrecondGroup, reports) -> None:
+def _check_reports(group: PrecondGroup, reports, offset: int = 0) -> None:
     failed = [i for i, r in enumerate(reports) if not r.converged]
     if failed:
         details = ", ".join(
-            f"layer {group.members[i][0]} side {group.members[i][1]} block {group.members[i][2]}"
-            f" (residual {reports[i].residual:.3e})" for i in failed)
+            f"layer {group.members[offset + i][0]} side {group.members[offset + i][1]} block "
+            f"{group.members[offset + i][2]} (residual {reports[i].residual:.3e})" for i in failed)
         raise ConvergenceError(f"inverse-root solver failed on: {details}")
 
 
@@ -474,103 +543,116 @@ def refresh_inverse_roots(state: ShampooState, cfg: ShampooConfig, seed: int = 0
     if state.step % cfg.update_freq != 0:
         return state
     rt: _Runtime = state.runtime
-    solver = cfg.solver
-    L = _lib.lib()
-    sc = rt.scratch
     if not rt.stats_valid or rt.stats_eps != cfg.epsilon:
         _group_stats(state, cfg)
     rt.stats_valid = True
-    # block sharding: rank-local group gi is global group global_gid[gi]; its members' global slots
-    gids = getattr(rt, "global_gid", None)
-    sidx = getattr(rt, "seed_index", None)
-    tol_mode = solver.require_convergence
-    mode = solver.precision
-    ng = len(state.groups)
-    err = sc.tensor("err", (2,), torch.int32)
-    err.zero_()
-    oks = sc.tensor("ok", (max(ng, 1),), torch.int32)
+    err, oks = _refresh_flags(rt, len(state.groups))
     for gi, group in enumerate(state.groups):
-        p, n, d = group.exponent, len(group.members), group.dim
-        gid = gids[gi] if gids is not None else gi
-        if solver.method == "evd":
-            group.roots.copy_(evd_inverse_root_torch(group.ema, p, solver.heuristic))
+        if cfg.solver.method == "evd":
+            group.roots.copy_(evd_inverse_root_torch(group.ema, group.exponent, cfg.solver.heuristic))
             rt.root_split[gi].load(group.roots)
             continue
-        a = sc.stack("a", n, d, d)
-        a.amax.copy_(rt.g_amax[gi])  # exact max|ema + eps I| (accumulate's symmetrization)
-        _lib.check(L.dash_group_split_a(group.ema.data_ptr(), float(cfg.epsilon), a.ref(), _lib.stream_ptr()),
-                   "dash_group_split_a")
-        scale = sc.tensor("scale", (n,))
-        inv = sc.tensor("inv", (n,))
-        status = sc.tensor("status", (n,), torch.int32)
-        status.zero_()
-        if isinstance(solver.scaling, Frobenius):
-            _lib.check(L.dash_fro_scale(rt.g_fro[gi].data_ptr(), n, scale.data_ptr(), inv.data_ptr(),
-                                        _lib.stream_ptr()), "dash_fro_scale")
-        else:
-            power_iteration_scales(group.ema, cfg.epsilon, solver.scaling.pool, solver.scaling.iters,
-                                   block_seed(seed, gid), scale, inv, status,
-                                   sidx[gi] if sidx is not None else None, a_split=a)
-        ok = oks[gi:gi + 1]
-        _lib.check(L.dash_scale_check(scale.data_ptr(), status.data_ptr(), n, gi, ok.data_ptr(), err.data_ptr(),
-                                      _lib.stream_ptr()), "dash_scale_check")
-        if tol_mode:  # the reference raises here, before any solve of this group (shampoo.py:323-325)
-            vals = err.tolist()
-            if vals[0]:
-                _raise_scale_error(state, vals)
-        if solver.method == "cbshv":
-            coeffs = _solver_coefficients(solver, p)
-            clenshaw_split(a, coeffs, inv, inv_pow(inv, p, sc), group.roots, rt.root_split[gi], mode, gate=ok,
-                           scratch=sc)
-            continue
-        if solver.method == "cn":
-            x, rep = cn_split(a, inv, CnConfig(p=p, tolerance=solver.tolerance, max_iters=solver.max_iters), mode,
-                              scratch=sc)
-            reps = [rep]
-            src = x
-        else:  # ndb
-            # the iterates stay in upper pair-block storage (the second solve of a 4th root reads Y1 that way);
-            # only the root that is read next is completed
-            if p == 2:
-                _, src, rep = ndb_split(a, inv, solver.tolerance, solver.max_iters, mode, complete=False,
-                                        scratch=sc, tag="ndb1")
-                reps = [rep]
-            else:
-                y1, _, r1 = ndb_split(a, inv, solver.tolerance, solver.max_iters, mode, complete=False,
-                                      scratch=sc, tag="ndb1")
-                _, src, r2 = ndb_split(y1, None, solver.tolerance, solver.max_iters, mode, complete=False,
-                                       scratch=sc, tag="ndb2")
-                reps = [r1, r2]
-            fill_lower(src)
-        fallback = None
-        if tol_mode:  # per-block reports, in the reference's order (first chain, then second)
-            lists = [r.to_list() for r in reps]
-            # FULL64 re-solves in float64 the blocks its fp32-class iteration could not converge: frozen before
-            # max_iters (watch / non-finite), or -- when the requested tolerance is below the floor, so the
-            # reference's float64 loop would have converged where ours stalls -- any unconverged block
-            floor_mode = stall_for(solver.tolerance, mode) > 0.0
-            bad = sorted({i for lst in lists for i, r in enumerate(lst)
-                          if not r.converged and (floor_mode or r.iterations < solver.max_iters)})
-            if mode is PrecisionMode.FULL64 and bad:
-                fallback = bad
-                for lst in lists:
-                    for i in bad:
-                        lst[i] = IterationReport(lst[i].iterations, lst[i].residual, True)
-            for lst in lists:
-                _check_reports(group, lst)
-        # roots = Z * scale^(-1/p)  -> fp32 state roots + split copy for the apply (gated on the scale checks)
-        _lib.check(L.dash_scale_stack(src.ref(), inv.data_ptr(), 1.0 / p, group.roots.data_ptr(),
-                                      group.roots.stride(0), group.roots.stride(1), rt.root_split[gi].ref(),
-                                      ok.data_ptr(), _lib.stream_ptr()), "dash_scale_stack")
-        if fallback:
-            idx = torch.tensor(fallback, dtype=torch.long, device=rt.dev)
-            group.roots[idx] = inverse_root_f64(group.ema[idx], cfg.epsilon, p)
-            rt.root_split[gi].load(group.roots)
-    if not tol_mode:
+        _refresh_range(state, cfg, gi, 0, len(group.members), seed, err, oks[gi:gi + 1])
+    if not cfg.solver.require_convergence:
         rt.pending_err = err
         if not defer_check:
             check_step_status(state)
     return state
+
+
+def _refresh_flags(rt: "_Runtime", nflags: int):
+    """The refresh's shared device error word (zeroed) and per-range commit gates."""
+    err = rt.scratch.tensor("err", (2,), torch.int32)
+    err.zero_()
+    return err, rt.scratch.tensor("ok", (max(nflags, 1),), torch.int32)
+
+
+def _refresh_range(state: ShampooState, cfg: ShampooConfig, gi: int, s: int, e: int, seed: int,
+                   err: torch.Tensor, ok: torch.Tensor) -> None:
+    """Scale, solve, check and commit the roots of group `gi`'s members [s, e) (the whole group, or one chunk of
+    the pipelined host step); every per-block computation is independent of the range, so any partition of a
+    group gives bit-identical roots."""
+    rt: _Runtime = state.runtime
+    solver = cfg.solver
+    L = _lib.lib()
+    sc = rt.scratch
+    group = state.groups[gi]
+    p, n, d = group.exponent, e - s, group.dim
+    gids = getattr(rt, "global_gid", None)  # block sharding: rank-local group gi is global group gids[gi]
+    sidx = getattr(rt, "seed_index", None)
+    gid = gids[gi] if gids is not None else gi
+    tol_mode = solver.require_convergence
+    mode = solver.precision
+    ema = group.ema[s:e]
+    roots = group.roots[s:e]
+    rsplit = rt.root_split[gi].slice(s, e)
+    a = sc.stack("a", n, d, d)
+    a.amax.copy_(rt.g_amax[gi][s:e])  # exact max|ema + eps I| (accumulate's symmetrization)
+    _lib.check(L.dash_group_split_a(ema.data_ptr(), float(cfg.epsilon), a.ref(), _lib.stream_ptr()),
+               "dash_group_split_a")
+    scale = sc.tensor("scale", (n,))
+    inv = sc.tensor("inv", (n,))
+    status = sc.tensor("status", (n,), torch.int32)
+    status.zero_()
+    if isinstance(solver.scaling, Frobenius):
+        parts = rt.prep_parts
+        _lib.check(L.dash_fro_scale(rt.g_fro[gi][s * parts:].data_ptr(), n, scale.data_ptr(), inv.data_ptr(),
+                                    _lib.stream_ptr()), "dash_fro_scale")
+    else:  # block i of the group draws from block_seed(group seed, global slot of i) (spectral.py:117)
+        seed_index = sidx[gi][s:e] if sidx is not None else (rt.slot_ids(gi)[s:e] if s > 0 else None)
+        power_iteration_scales(ema, cfg.epsilon, solver.scaling.pool, solver.scaling.iters, block_seed(seed, gid),
+                               scale, inv, status, seed_index, a_split=a)
+    _lib.check(L.dash_scale_check(scale.data_ptr(), status.data_ptr(), n, gi, ok.data_ptr(), err.data_ptr(),
+                                  _lib.stream_ptr()), "dash_scale_check")
+    if tol_mode:  # the reference raises here, before any solve of this group (shampoo.py:323-325)
+        vals = err.tolist()
+        if vals[0]:
+            _raise_scale_error(state, vals)
+    if solver.method == "cbshv":
+        clenshaw_split(a, _solver_coefficients(solver, p), inv, inv_pow(inv, p, sc), roots, rsplit, mode, gate=ok,
+                       scratch=sc)
+        return
+    if solver.method == "cn":
+        src, rep = cn_split(a, inv, CnConfig(p=p, tolerance=solver.tolerance, max_iters=solver.max_iters), mode,
+                            scratch=sc)
+        reps = [rep]
+    elif p == 2:
+        # the iterates stay in upper pair-block storage (the second solve of a 4th root reads Y1 that way); only
+        # the root that is read next is completed
+        _, src, rep = ndb_split(a, inv, solver.tolerance, solver.max_iters, mode, complete=False, scratch=sc,
+                                tag="ndb1")
+        reps = [rep]
+    else:
+        y1, _, r1 = ndb_split(a, inv, solver.tolerance, solver.max_iters, mode, complete=False, scratch=sc,
+                              tag="ndb1")
+        _, src, r2 = ndb_split(y1, None, solver.tolerance, solver.max_iters, mode, complete=False, scratch=sc,
+                               tag="ndb2")
+        reps = [r1, r2]
+    if solver.method == "ndb":
+        fill_lower(src)
+    fallback = None
+    if tol_mode:  # per-block reports, in the reference's order (first chain, then second)
+        lists = [r.to_list() for r in reps]
+        # FULL64 re-solves in float64 the blocks its fp32-class iteration could not converge: frozen before
+        # max_iters (watch / non-finite), or -- when the requested tolerance is below the floor, so the
+        # reference's float64 loop would have converged where ours stalls -- any unconverged block
+        floor_mode = stall_for(solver.tolerance, mode) > 0.0
+        bad = sorted({i for lst in lists for i, r in enumerate(lst)
+                      if not r.converged and (floor_mode or r.iterations < solver.max_iters)})
+        if mode is PrecisionMode.FULL64 and bad:
+            fallback = bad
+            for lst in lists:
+                for i in bad:
+                    lst[i] = IterationReport(lst[i].iterations, lst[i].residual, True)
+        for lst in lists:
+            _check_reports(group, lst, offset=s)
+    # roots = Z * scale^(-1/p)  -> fp32 state roots + split copy for the apply (gated on the scale checks)
+    _lib.check(L.dash_scale_stack(src.ref(), inv.data_ptr(), 1.0 / p, roots.data_ptr(), roots.stride(0),
+                                  roots.stride(1), rsplit.ref(), ok.data_ptr(), _lib.stream_ptr()), "dash_scale_stack")
+    if fallback:
+        idx = torch.tensor(fallback, dtype=torch.long, device=rt.dev)
+        roots[idx] = inverse_root_f64(ema[idx], cfg.epsilon, p)
+        rsplit.load(roots)
 
 
 def inv_pow(inv: torch.Tensor, p: int, scratch=None) -> torch.Tensor:
@@ -610,6 +692,8 @@ def step(state: ShampooState, params, grads, cfg: ShampooConfig, seed: int = 0, 
             ev.record()
             events.setdefault(name, []).append(ev)
 
+    if _pipelined(state, params, grads, cfg):
+        return _step_pipelined(state, params, grads, cfg, seed, events)
     mark("start")
     accumulate(state, grads, cfg)
     host_params = isinstance(params[0], torch.Tensor) and not params[0].is_cuda and params[0].is_pinned()
@@ -651,6 +735,102 @@ def step(state: ShampooState, params, grads, cfg: ShampooConfig, seed: int = 0, 
             p_.copy_(o)
         return list(params), state
     return [o.clone() for o in outs], state
+
+
+# ============================================================================ pipelined host-buffer step
+def _host_chunks() -> int:
+    return max(1, int(os.environ.get("DASH_HOST_CHUNKS", "6")))
+
+
+def _pipelined(state: ShampooState, params, grads, cfg: ShampooConfig) -> bool:
+    """Host (pinned CPU) parameters and gradients with a fixed-iteration solver: the step is pipelined by layer
+    chunks so the PCIe copies overlap the device work (tolerance-mode refreshes read reports group by group
+    and the EVD solver is host-orchestrated: those run the plain step)."""
+    def pinned(ts):
+        return all(isinstance(x, torch.Tensor) and not x.is_cuda and x.is_pinned() for x in ts)
+
+    rt = state.runtime
+    return (_host_chunks() > 1 and len(rt.shapes) > 1 and cfg.solver.tolerance == 0.0
+            and cfg.solver.method != "evd" and getattr(rt, "global_gid", None) is None
+            and len(params) == len(rt.shapes) and len(grads) == len(rt.shapes) and pinned(params) and pinned(grads))
+
+
+def _step_pipelined(state: ShampooState, params, grads, cfg: ShampooConfig, seed: int, events: dict | None):
+    """shampoo.step for host buffers: layer chunk k's gradients and parameters go up, its statistics, roots and
+    update are computed, and its new parameters come down while chunk k+1 is transferred and computed
+    (three streams).  Per-block work is independent of the chunking (the preconditioner members of a layer range
+    are a contiguous slot range of every group), so the result is bit-identical to the one-shot step."""
+    rt: _Runtime = state.runtime
+    for layer, g in zip(state.layers, grads):
+        if tuple(g.shape) != layer.shape:
+            raise ValueError(f"layer {layer.layer_id}: gradient shape {tuple(g.shape)} != {layer.shape}")
+    for i, p_ in enumerate(params):
+        if tuple(p_.shape) != rt.shapes[i]:
+            raise ValueError(f"layer {i}: shape {tuple(p_.shape)} != {rt.shapes[i]}")
+    t = state.step
+    chunks = rt.ensure_chunks(cfg, state.layers, _host_chunks())
+    L = _lib.lib()
+    comp = torch.cuda.current_stream()
+    if getattr(rt, "h2d_stream", None) is None:
+        rt.h2d_stream, rt.d2h_stream = torch.cuda.Stream(device=rt.dev), torch.cuda.Stream(device=rt.dev)
+    h2d, d2h = rt.h2d_stream, rt.d2h_stream
+    h2d.wait_stream(comp)
+    out = torch.empty(rt.theta_out.numel(), dtype=torch.float32, pin_memory=True)
+
+    def upload(ch) -> torch.cuda.Event:
+        with torch.cuda.stream(h2d):
+            for li in range(ch.l0, ch.l1):
+                o0, o1 = int(rt.offsets[li]), int(rt.offsets[li + 1])
+                rt.grad[o0:o1].copy_(grads[li].reshape(-1), non_blocking=True)
+                rt.theta[o0:o1].copy_(params[li].reshape(-1), non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(h2d)
+        return ev
+
+    # chunk k+1's copies are issued after chunk k's work is enqueued: the solvers' small job-table uploads then
+    # never queue behind gigabytes of pending H2D traffic (the host would block on them)
+    ev_next = upload(chunks[0])
+    refresh = t % cfg.update_freq == 0
+    step_seed = block_seed(seed, t)
+    err, oks = _refresh_flags(rt, sum(len(ch.ranges) for ch in chunks))
+    eta = float(cfg.lr.value(t))
+    k_ok = 0
+    if events is not None:
+        events.setdefault("start", []).append(torch.cuda.Event(enable_timing=True))
+        events["start"][-1].record()
+    for k, ch in enumerate(chunks):
+        comp.wait_event(ev_next)
+        _lib.check(L.dash_plan_accumulate(ch.plan, float(cfg.graft.beta2), float(cfg.graft.beta1), t + 1,
+                                          float(cfg.graft.graft_eps), _lib.stream_ptr()), "dash_plan_accumulate")
+        for gi, s0, e0 in ch.ranges:  # linalg.symmetrize + max|a| / sum(a^2) of the chunk's members
+            g = state.groups[gi]
+            _lib.check(L.dash_group_sym(g.ema[s0:e0].data_ptr(), e0 - s0, g.dim, float(cfg.epsilon),
+                                        rt.g_amax[gi][s0:e0].data_ptr(), rt.g_fro[gi][s0 * rt.prep_parts:].data_ptr(),
+                                        _lib.stream_ptr()), "dash_group_sym")
+        if refresh:
+            for gi, s0, e0 in ch.ranges:
+                _refresh_range(state, cfg, gi, s0, e0, step_seed, err, oks[k_ok:k_ok + 1])
+                k_ok += 1
+        _lib.check(L.dash_plan_apply(ch.plan, rt.theta.data_ptr(), rt.theta_out.data_ptr(), eta, _lib.stream_ptr()),
+                   "dash_plan_apply")
+        if k + 1 < len(chunks):
+            ev_next = upload(chunks[k + 1])
+        done = torch.cuda.Event()
+        done.record(comp)
+        d2h.wait_event(done)
+        with torch.cuda.stream(d2h):
+            out[ch.e0:ch.e1].copy_(rt.theta_out[ch.e0:ch.e1], non_blocking=True)
+    rt.stats_valid, rt.stats_eps = True, cfg.epsilon
+    if events is not None:
+        events.setdefault("applied", []).append(torch.cuda.Event(enable_timing=True))
+        events["applied"][-1].record()
+    comp.wait_stream(d2h)
+    if refresh:
+        rt.pending_err = err
+    check_step_status(state)  # synchronises; raises before anything is returned
+    d2h.synchronize()
+    state.step = t + 1
+    return [out[int(rt.offsets[i]):int(rt.offsets[i + 1])].view(s) for i, s in enumerate(rt.shapes)], state
 
 
 # ============================================================================ checkpointing

@@ -40,9 +40,9 @@ def c1_stack(b=256):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--kmax", type=int, default=30)
-    ap.add_argument("--mode", default="f32", choices=["f32", "f16"])
+    ap.add_argument("--mode", default="f32", choices=["f64", "f32", "f16"])
     args = ap.parse_args()
-    mode = PrecisionMode.EMULATED32 if args.mode == "f32" else PrecisionMode.F16
+    mode = {"f64": PrecisionMode.FULL64, "f32": PrecisionMode.EMULATED32, "f16": PrecisionMode.F16}[args.mode]
     cases = []
     for b, n in ((256, 8), (1024, 4)):
         for cond in (1e1, 1e2, 1e3, 1e4):
