@@ -567,6 +567,68 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_train(args):
+    """Config 5's full training step on one GPU: Llama-953M forward + backward (bf16 autocast, fp32 master
+    weights, synthetic tokens) and the DASH step on its gradients (NDB fixed iters, PI, B = 1024)."""
+    import torch
+
+    from paper_2602_02016_b200 import _lib
+    from paper_2602_02016_b200.linalg import PrecisionMode
+    from paper_2602_02016_b200.llama import LlamaShape, TrainStep
+    from paper_2602_02016_b200.shampoo import ShampooConfig, SolverConfig
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    shape = LlamaShape()
+    prec = {"f32": PrecisionMode.EMULATED32, "f16": PrecisionMode.F16}[args.precision]
+    cfg = ShampooConfig(block_size=1024, solver=SolverConfig(method=args.solver, tolerance=0.0, max_iters=args.iters,
+                                                             precision=prec))
+    trainer = TrainStep(shape, cfg, "cuda", seed=0)
+    batch, seq = args.batch, args.seq
+    g = torch.Generator().manual_seed(0)
+    host_tokens = [torch.randint(0, shape.vocab, (batch, seq + 1), generator=g).pin_memory() for _ in range(2)]
+    dev_tokens = [t.cuda() for t in host_tokens]
+    for i in range(args.warmup):
+        trainer(dev_tokens[i % 2])
+    torch.cuda.synchronize()
+    events: dict = {}
+    launches0 = _lib.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        torch.cuda.synchronize()
+        ev0.record()
+        for i in range(args.steps):
+            loss = trainer(dev_tokens[i % 2], events=events)
+        ev1.record()
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    launches = (_lib.launch_count() - launches0) // args.steps
+    fwd_bwd = statistics.mean(a.elapsed_time(b) for a, b in zip([ev0] + events["applied"][:-1], events["backward_done"]))
+    opt = statistics.mean(a.elapsed_time(b) for a, b in zip(events["backward_done"], events["applied"]))
+    # end to end: the caller's token batch from pinned host memory, the loss read back every step
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        loss = trainer(host_tokens[i % 2].cuda(non_blocking=True))
+        float(loss)
+    torch.cuda.synchronize()
+    e2e = (time.perf_counter() - t0) / args.steps * 1e3
+    tokens = batch * seq
+    print(json.dumps({
+        "metric": METRIC, "value": round(ms, 3), "unit": "ms", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16 model fwd/bwd (fp32 master), fp16x3-split DASH products",
+        "data": "synthetic tokens (uniform over the vocabulary), random-init Llama-953M",
+        "config": {"workload": f"llama953m-train: full training step (fwd + bwd + DASH, B=1024, "
+                               f"{SOLVER_DESC[args.solver].format(k=args.iters)}, PI)", "global_batch": batch,
+                   "seq_len": seq, "tokens_per_step": tokens, "parallelism": "single GPU"},
+        "phases_ms": {"forward_backward": round(fwd_bwd, 3), "dash_step": round(opt, 3)},
+        "tokens_per_s": round(tokens / (ms * 1e-3), 1), "final_loss": float(loss), "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "e2e": {"value": round(e2e, 3), "unit": "ms", "h2d_bytes_per_step": tokens * 8 + batch * 8,
+                "d2h_bytes_per_step": 4},
+    }), flush=True)
+
+
 def spawn_ranks(args) -> int:
     """`--gpus N` without a torchrun environment: re-launch this script under torchrun with N local ranks."""
     import torch
@@ -586,7 +648,9 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["dash", "reference"], default="dash")
-    ap.add_argument("--workload", default="llama953m", choices=["llama953m", "llama124m", "c1"])
+    ap.add_argument("--workload", default="llama953m", choices=["llama953m", "llama124m", "c1", "llama953m-train"])
+    ap.add_argument("--batch", type=int, default=4, help="llama953m-train: sequences per step")
+    ap.add_argument("--seq", type=int, default=1024, help="llama953m-train: tokens per sequence")
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--precision", default="f32", choices=["f32", "f16"])
     ap.add_argument("--solver", default="ndb", choices=["ndb", "cn", "cbshv"])
@@ -603,6 +667,8 @@ def main():
               file=sys.stderr)
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "llama953m-train":
+        run_train(args)
     else:
         run_dash(args)
 
