@@ -323,9 +323,16 @@ def run_dash(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # DASH_DIST_BACKEND=gloo: ranks may share a GPU (exchange staged through the host) -- a functional check of
+    # the sharded path on a one-GPU box; the measured multi-GPU runs use NCCL, one rank per GPU
+    backend = os.environ.get("DASH_DIST_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     shapes, bsz = workload_shapes(args.workload)
     prec = {"f32": PrecisionMode.EMULATED32, "f16": PrecisionMode.F16}[args.precision]
     cfg = ShampooConfig(block_size=bsz, solver=SolverConfig(method=args.solver, tolerance=0.0,
@@ -468,7 +475,8 @@ def run_dash(args):
                         f"PI scaling (pool 16 x 30 iters), update_freq=1, grafting beta2=0.999",
             "params": int(sum(int(np.prod(s)) for s in shapes)),
             "precond_blocks": None,
-            "parallelism": f"block-sharded x{world}" if world > 1 else "single GPU",
+            "parallelism": (f"block-sharded x{world} ({os.environ.get('DASH_DIST_BACKEND', 'nccl')})" if world > 1
+                            else "single GPU"),
             "l2": "working set (EMA/roots/iterates, GBs) >> 126 MB L2; no explicit flush",
             "solver_precision": args.precision,
         },
