@@ -81,7 +81,8 @@ int dash_bmm(const dash_stack* a, int trans_a, const dash_stack* b, int trans_b,
  * (inv_scale may be NULL = 1), i.e. the reference's a / scales (shampoo.py:326).  Per-block reports are
  * written to device arrays iters[N], resid[N] (float), conv[N] (0/1) exactly as IterationReport
  * (roots.py:32-36).  tol = 0 is fixed-iteration mode.  passes: 3 = split-f16 (fp32-class), 4 = split-f16
- * with four K-range accumulators per tile (FULL64: ~2.5x smaller accumulation error, ~11% slower), 1 = fp16.
+ * accumulated in 16 K ranges per tile, each drained from TMEM into fp32 registers (FULL64: B = 1024 Newton-DB
+ * error ~14x smaller, ~20% slower), 1 = fp16.
  * stall > 0 (used when the requested tolerance is below the rounding floor of the arithmetic): a block whose
  * residual stops decreasing (r_k >= r_{k-1}) once r_{k-1} <= stall is frozen as converged at that floor;
  * stall = 0 keeps the reference's rules exactly (non-finite, r <= tol, divergence watch).

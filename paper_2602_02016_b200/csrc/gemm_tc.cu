@@ -115,7 +115,8 @@ __device__ __forceinline__ void store_split(__half* hi, long long plane, int ld,
 // 128 x 128 sub-block twice (direct and transposed) and drops the one below-diagonal sub-block of each
 // diagonal tile, so every output element has exactly one writer (deterministic).
 constexpr int kPairM = kTileM, kHalf = kTileM / 2;
-constexpr int kNaccDefault = 2;   // split-f16 accumulators per tile (env DASH_NACC = 1, 2 = main + correction, 4)
+constexpr int kNaccDefault = 2;   // split-f16 accumulators per tile (env DASH_NACC = 1, 2 = main + correction,
+                                   // 4 = three K-range mains + correction, 8 / 16 = ring of that many K ranges)
 constexpr int kEpiWarps = 8;     // 2 per TMEM lane quarter, 64 columns each
 constexpr int kSlots = 4;         // TMEM accumulator slots (4 x 128 columns = all 512)
 constexpr int kRing = 8;          // tile-index ring shared by the pair (dynamic scheduling)
@@ -466,8 +467,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
   constexpr int kPN = NT;                    // pair tile columns = TMEM columns per accumulator slot
   constexpr int kRounds = NT / 128;          // epilogue passes over a tile (128 columns each)
   constexpr uint32_t kSl = 512 / NT;         // TMEM slots
-  const int nacc = NT == 128 ? (nacc_in & 0xff) : 1;  // accumulators per tile (1, 2 or 4; 1 for NT = 256)
+  const int nacc_req = NT == 128 ? (nacc_in & 0xff) : 1;
+  // ring mode (split products, nacc_req = R >= 8): the K loop of a tile is cut into R ranges ("units"); unit u of
+  // the launch accumulates in TMEM slot u % 4 and the epilogue adds it into registers (fp32, round to nearest)
+  // and releases the slot, so each truncating tensor-core accumulation chain is K / R long while the four slots
+  // keep the MMA running ahead of the epilogue
+  const bool ring = PASSES == 3 && nacc_req >= 8;
+  const int nring = ring ? nacc_req : 0;
+  const int nacc = ring ? static_cast<int>(kSl) : nacc_req;  // accumulators per tile (1, 2 or 4; 1 for NT = 256)
   const bool mc = PASSES == 3 && nacc == 2;  // main (hi*hi) + correction (hi*lo + lo*hi) accumulators
+  const bool mc4 = PASSES == 3 && nacc == 4 && !ring;  // three K-range main accumulators + correction
   const int xp = nacc_in >> 8;  // DASH_EXP knobs: timing 1 hi planes only, 2 no epilogue, 4 no staging, 8 no bulk stores, 16 L2 prefetch; 32 mirror via global stores (valid, 2-3% slower); 64 / 128 plain (unhinted) split stores / operand loads
   const uint32_t nsets = kSl / nacc;         // tiles in flight in TMEM
 
@@ -633,6 +642,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t t = 0;
+      uint32_t ucount = 0;  // ring mode: accumulation units issued so far
       for (;; ++t) {
         int tile = 0;
         if (lane == 0) tile = next_tile(t);
@@ -644,22 +654,71 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         tile_coords<NT>(jb, tile - job_tile_start<NT>(jb), ti, tj);
         const int a_up = KB == 64 ? jb.a_up : 0, b_up = KB == 64 ? jb.b_up : 0;
         const int bpb = (tj * kPN) >> 8;  // 256-block of this tile's B rows (the same for both CTAs)
-        // main + correction mode (nacc == 2, split products): hi*hi -> slot 0, hi*lo + lo*hi -> slot 1 over the
-        // whole K; otherwise slot c takes the k-blocks [c*per, (c+1)*per)
-        const int per = mc ? nk : (nk + nacc - 1) / nacc;
+        // Split products keep the cross terms hi*lo + lo*hi (2^-11 smaller) in their own "correction" slot, the
+        // last one of the tile, so they never truncate against the full-size sum.  The hi*hi terms go to
+        // `nmain` slots by K range: nacc == 2 -> one main slot over the whole K; nacc == 4 -> three main slots of
+        // K / 3 each (shorter truncating accumulation chains, FULL64).  Unsplit products (fp16, or DASH_NACC=1)
+        // put every pass into slot c = K range c of nacc.
+        if (ring) {  // ---- ring mode: units of per_u k-blocks, unit u -> slot u % kSl
+          const int per_u = (nk + nring - 1) / nring;
+          for (int kb = 0; kb < nk; ++kb) {
+            const bool first = kb % per_u == 0;
+            const uint32_t u = ucount + static_cast<uint32_t>(kb / per_u);
+            const uint32_t slot = u % kSl;
+            if (first) {
+              const long long w0 = prof ? clock64() : 0;
+              mbar_wait(&tempty[slot], ((u / kSl) & 1u) ^ 1u);
+              if (prof) pw0 += clock64() - w0;
+              tc_fence_after();
+            }
+            const int a_mn = jb.a_mn ^ static_cast<int>(a_up && upper_flip(jb.a_mn, ti, (kb * KB) >> 8));
+            const int b_mn = jb.b_mn ^ static_cast<int>(b_up && upper_flip(jb.b_mn, bpb, (kb * KB) >> 8));
+            const uint32_t idesc = umma_idesc_f16(kPairM, kPN, a_mn, b_mn);
+            const uint32_t a_lbo = a_mn ? KB * 128u : 16u, b_lbo = b_mn ? KB * 128u : 16u;
+            const uint32_t a_kstep = a_mn ? 2048u : 32u, b_kstep = b_mn ? 2048u : 32u;
+            const uint32_t a_sbo = a_mn ? 1024u : (KB == 64 ? 1024u : 512u), b_sbo = b_mn ? 1024u : (KB == 64 ? 1024u : 512u);
+            const uint32_t a_lay = a_mn ? 2u : (KB == 64 ? 2u : 4u), b_lay = b_mn ? 2u : (KB == 64 ? 2u : 4u);
+            {
+              const long long w0 = prof ? clock64() : 0;
+              mbar_wait(&full[stage], phase);
+              if (prof) pw1 += clock64() - w0;
+            }
+            tc_fence_after();
+            const uint32_t a_base = smem_u32(smem + stage * C::kStageBytes);
+            const uint32_t b_base = a_base + C::kABytes * C::kPlanes;
+#pragma unroll
+            for (int k = 0; k < KB / 16; ++k) {
+#pragma unroll
+              for (int p = 0; p < PASSES; ++p) {
+                const uint32_t ap = (p == 2) ? 1u : 0u, bp = (p == 1) ? 1u : 0u;
+                const uint64_t ad = umma_sdesc(a_base + ap * C::kABytes + k * a_kstep, a_lbo, a_sbo, a_lay);
+                const uint64_t bd = umma_sdesc(b_base + bp * C::kBBytes + k * b_kstep, b_lbo, b_sbo, b_lay);
+                umma2_f16_elect(tmem_base + slot * kPN, ad, bd, idesc, (first && k == 0 && p == 0) ? 0u : 1u);
+              }
+            }
+            umma2_commit_mc_elect(&empty[stage]);
+            if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+            if (kb % per_u == per_u - 1 || kb == nk - 1) umma2_commit_mc_elect(&tfull[slot]);
+          }
+          ucount += static_cast<uint32_t>((nk + per_u - 1) / per_u);
+          continue;
+        }
+        const int nmain = mc ? 1 : (mc4 ? 3 : nacc);
+        const int per = (nk + nmain - 1) / nmain;  // k-blocks per main slot
+        const bool corr = mc || mc4;
         // K-major: 128-byte (KB 64) or 64-byte (KB 32) swizzled rows, 8-row groups 1024 / 512 B apart, 32 B per
         // 16-wide k step; MN-major: 128-byte rows along M/N, 64-column groups KB * 128 B apart, 2 KB per k step
         constexpr uint32_t kSbo = KB == 64 ? 1024u : 512u, kLay = KB == 64 ? 2u : 4u;
         const uint32_t base = (t % nsets) * static_cast<uint32_t>(nacc);
+        const uint32_t corr_slot = base + static_cast<uint32_t>(nacc - 1);
         const uint32_t use_par = ((t / nsets) & 1u) ^ 1u;
-        int c = 0, kin = 0;  // accumulator slot, k-block index within the slot's K range
         for (int kb = 0; kb < nk; ++kb) {
-          const bool first = kin == 0;
-          const uint32_t slot = base + static_cast<uint32_t>(c);
-          if (first) {
+          const bool first = kb % per == 0;
+          const uint32_t slot = base + static_cast<uint32_t>(kb / per);
+          if (first || (corr && kb == 0)) {
             const long long w0 = prof ? clock64() : 0;
-            mbar_wait(&tempty[slot], use_par);
-            if (mc) mbar_wait(&tempty[slot + 1], use_par);
+            if (first) mbar_wait(&tempty[slot], use_par);
+            if (corr && kb == 0) mbar_wait(&tempty[corr_slot], use_par);
             if (prof) pw0 += clock64() - w0;
             tc_fence_after();
           }
@@ -688,24 +747,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
               const uint32_t bp = (p == 1) ? 1u : 0u;  // pass 1: A_hi * B_lo
               const uint64_t ad = umma_sdesc(a_base + ap * C::kABytes + k * a_kstep, a_lbo, a_sbo, a_lay);
               const uint64_t bd = umma_sdesc(b_base + bp * C::kBBytes + k * b_kstep, b_lbo, b_sbo, b_lay);
-              // main + correction mode: passes 1, 2 go to the next slot, whose first write is pass 1
-              const uint32_t fresh = (first && k == 0 && (p == 0 || (mc && p == 1))) ? 0u : 1u;
-              umma2_f16_elect(d_tmem + ((mc && p) ? static_cast<uint32_t>(kPN) : 0u), ad, bd, idesc, fresh);
+              const bool to_corr = corr && p > 0;
+              // a slot's first write overwrites (main: pass 0 of its first k step; correction: pass 1 of k-block 0)
+              const uint32_t fresh = to_corr ? ((kb == 0 && k == 0 && p == 1) ? 0u : 1u)
+                                             : ((first && k == 0 && p == 0) ? 0u : 1u);
+              umma2_f16_elect(to_corr ? tmem_base + corr_slot * kPN : d_tmem, ad, bd, idesc, fresh);
             }
           }
           umma2_commit_mc_elect(&empty[stage]);
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
-          if (++kin == per || kb == nk - 1) {
-            umma2_commit_mc_elect(&tfull[slot]);  // this slot's K range is complete
-            ++c;
-            if (mc) {
-              umma2_commit_mc_elect(&tfull[slot + 1]);
-              ++c;
-            }
-            kin = 0;
-          }
+          if (kb % per == per - 1 || kb == nk - 1) umma2_commit_mc_elect(&tfull[slot]);  // K range complete
+          if (corr && kb == nk - 1) umma2_commit_mc_elect(&tfull[corr_slot]);
         }
-        for (; c < nacc; ++c) {  // slots without k-blocks (nk < nacc): keep every slot's phase in step
+        // main slots without k-blocks (nk < nmain): keep every slot's phase in step
+        for (int c = (nk + per - 1) / per; c < nmain; ++c) {
           const uint32_t slot = base + static_cast<uint32_t>(c);
           mbar_wait(&tempty[slot], use_par);
           tc_fence_after();
@@ -732,6 +787,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       else tma_store_4d(maps + map, ebuf, x0, x1, 0, mat);
     };
     uint32_t t = 0;
+    uint32_t ucount = 0;  // ring mode: accumulation units drained so far
     for (;; ++t) {
       int tile = 0;
       if (lane == 0) tile = next_tile(t);
@@ -746,8 +802,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       for (int rd = 0; rd < kRounds; ++rd) {
         const int n0 = tj * kPN + 128 * rd;
         const int nk = (jb.K + KB - 1) / KB;
-        const int per = mc ? nk : (nk + nacc - 1) / nacc;
-        const int used = mc ? 2 : (nk + per - 1) / per;
+        const int nmain = mc ? 1 : (mc4 ? 3 : nacc);
+        const int per = (nk + nmain - 1) / nmain;
+        const int used_main = (nk + per - 1) / per;  // main slots with k-blocks; the correction slot is the last
         const uint32_t base = (t % nsets) * static_cast<uint32_t>(nacc);
         const uint32_t use_par = (t / nsets) & 1u;
         const bool side_tma = jb.s_map >= 0;
@@ -766,7 +823,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
           }
         }
         float acc[64];
-        for (int c = 0; c < nacc; ++c) {
+        // ring mode: drain the tile's units in issue order (unit u -> slot u % kSl), summing in registers
+        const int nunits = ring ? (nk + (nk + nring - 1) / nring - 1) / ((nk + nring - 1) / nring) : nacc;
+        for (int c = 0; c < nunits; ++c) {
+          if (ring) {
+            const uint32_t u = ucount + static_cast<uint32_t>(c), slot = u % kSl;
+            const long long w0 = prof ? clock64() : 0;
+            mbar_wait(&tfull[slot], (u / kSl) & 1u);
+            if (prof) pw0 += clock64() - w0;
+            tc_fence_after();
+            const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + slot * kPN + 64 * hc;
+  #pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              float v[32];
+              tmem_ld32(taddr + 32 * j, v);
+  #pragma unroll
+              for (int i = 0; i < 32; ++i) acc[32 * j + i] = (c == 0) ? v[i] : acc[32 * j + i] + v[i];
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote_relaxed(leader_tempty + slot * 8);
+            continue;
+          }
           const uint32_t slot = base + static_cast<uint32_t>(c);
           if (rd == 0) {
             const long long w0 = prof ? clock64() : 0;
@@ -774,7 +852,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             if (prof) pw0 += clock64() - w0;
             tc_fence_after();
           }
-          if (c < used) {
+          if (c < used_main || ((mc || mc4) && c == nacc - 1)) {
             const uint32_t taddr =
                 tmem_base + (static_cast<uint32_t>(q * 32) << 16) + slot * kPN + 128 * rd + 64 * hc;
   #pragma unroll
@@ -791,6 +869,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             if (lane == 0) mbar_arrive_remote_relaxed(leader_tempty + slot * 8);
           }
         }
+        if (ring) ucount += static_cast<uint32_t>(nunits);
         // ---- fused epilogue on the fp32 sums
         EpiCtx cx;
         cx.op = jb.op;
@@ -1041,12 +1120,13 @@ int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtenso
                 const GemmWide* wide) {
   if (total_tiles <= 0) return 0;
   if (!counter) return 1;
-  // passes = 4: the split 3-pass products with four K-range accumulators per tile (the FULL64 mode: ~2.5x
-  // smaller accumulation error, one tile in flight instead of two); otherwise the DASH_NACC default
+  // passes = 4: the split 3-pass products in ring mode with 16 K ranges per tile (FULL64: each truncating
+  // tensor-core accumulation chain covers K / 16; B = 1024 Newton-DB error ~14x smaller than the main +
+  // correction default, ~20% slower); otherwise the DASH_NACC default
   int nacc_req = 0;
   if (passes == 4) {
     passes = 3;
-    nacc_req = 4;
+    nacc_req = 16;
     issued *= 0.75;
   }
   const int wm = wide_mode();
@@ -1087,7 +1167,7 @@ int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtenso
   if (g_nacc == 0) {
     const char* e = getenv("DASH_NACC");
     g_nacc = e ? atoi(e) : kNaccDefault;
-    if (g_nacc != 1 && g_nacc != 2 && g_nacc != 4) g_nacc = kNaccDefault;
+    if (g_nacc != 1 && g_nacc != 2 && g_nacc != 4 && g_nacc != 8 && g_nacc != 16) g_nacc = kNaccDefault;
   }
   int num_sms = 0;
   cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, current_device());

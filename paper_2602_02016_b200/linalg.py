@@ -9,8 +9,9 @@ Precision modes (the reference has FULL64 / EMULATED32; the B200 build adds F16)
 * ``EMULATED32`` ("f32") -- split-f16 products: each operand is stored as fp16 hi + fp16 lo with a
   per-matrix power-of-two exponent, and every product issues hi*hi + hi*lo + lo*hi on the tensor
   cores with fp32 accumulation (22-bit significands, fp32-class results).
-* ``FULL64`` ("f64", the reference's default) -- the same split-f16 products with four K-range fp32
-  accumulators per output tile (about 2.5x smaller accumulation error than EMULATED32, ~11% slower); its
+* ``FULL64`` ("f64", the reference's default) -- the same split-f16 products, accumulated in 16 K ranges per
+  output tile that the epilogue sums in fp32 registers (tcgen05's fp32 accumulation truncates, so the error
+  grows with the chain length: B = 1024 Newton-DB error ~14x smaller than EMULATED32, ~20% slower); its
   Newton iterations converge at the fp32-class floor and blocks they cannot converge are re-solved in float64
   (see below).  Parity against the float64 reference is by the tolerances stated in DESIGN.md, never bitwise.
 * ``F16`` ("f16") -- hi*hi only (fp16 tensor rate, ~11-bit significands).
@@ -38,7 +39,7 @@ class PrecisionMode(enum.Enum):
 
 def passes_for(mode: PrecisionMode) -> int:
     """The engine's `passes` argument: 1 = fp16 products, 3 = split-f16 (hi*hi + hi*lo + lo*hi, main and
-    correction accumulators), 4 = the same split with four K-range accumulators per tile (FULL64)."""
+    correction accumulators), 4 = the same split accumulated in 16 K ranges per tile (FULL64)."""
     return {PrecisionMode.F16: 1, PrecisionMode.EMULATED32: 3, PrecisionMode.FULL64: 4}[mode]
 
 

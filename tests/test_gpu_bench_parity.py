@@ -108,3 +108,22 @@ def test_c2_chebyshev_256_blocks_vs_oracle(b, cond):
     errs = [relf(out[i], want[k]) for k, i in enumerate(SAMPLE)]
     print(f"C2 Chebyshev B={b} cond={cond:g}: {[f'{e:.1e}' for e in errs]}")
     assert max(errs) < 1e-3
+
+
+def _inv_sqrt(a):
+    w, q = np.linalg.eigh(a)
+    return (q / np.sqrt(w)[..., None, :]) @ np.swapaxes(q, -1, -2)
+
+
+@pytest.mark.parametrize("mode,tol", [(PrecisionMode.FULL64, 1.5e-5), (PrecisionMode.EMULATED32, 2e-4)])
+def test_ndb_accuracy_b1024_cond100_vs_eigh(mode, tol):
+    """Converged Newton-DB (12 iterations) on B = 1024, cond 1e2 blocks against the float64 eigh inverse square
+    root: FULL64 accumulates each product in 16 K ranges (ring mode) and reaches the 1e-5 class; EMULATED32
+    (main + correction accumulators, the benchmark's mode) ~1.4e-4 (profiles/r2_ring.log)."""
+    a = np.stack([core.random_spd(1024, 1e2, seed=i, scale=0.5) for i in range(4)])
+    _, z, _ = roots.batched_newton_db(torch.as_tensor(a, dtype=torch.float32, device="cuda"),
+                                      roots.NdbConfig(tolerance=0.0, max_iters=12), mode)
+    ref = _inv_sqrt(a)
+    err = max(relf(z[i].double().cpu().numpy(), ref[i]) for i in range(4))
+    print(f"NDB B=1024 cond 1e2 {mode.value}: Z relF vs eigh {err:.2e}")
+    assert err < tol

@@ -187,8 +187,11 @@ def test_c1_config_fixed_iterations_vs_oracle():
     ocfg = core.OracleConfig(block_size=256, method="ndb", tolerance=0.0, max_iters=10)
     ost = core.init_state([w], ocfg)
     oout, ost, _ = core.step(ost, [w], [g], ocfg, seed=0)
-    # literal C1 blocks have cond ~1e6 after one EMA step: fp32-class update error ~1e-2
-    assert relf(out[0] - w, oout[0] - w) < 2e-2
+    # literal C1 blocks have cond ~1e6 after one EMA step; FULL64 (the default precision) runs
+    # the statistics, solver and apply products in 16 K ranges per tile
+    err = relf(out[0] - w, oout[0] - w)
+    print(f"C1 fixed-10 update relF {err:.2e}")
+    assert err < 5e-3
     # the update norm identity holds per block regardless of conditioning
     assert np.linalg.norm(out[0] - w) == pytest.approx(np.linalg.norm(oout[0] - w), rel=1e-4)
 

@@ -48,10 +48,10 @@ def main() -> None:
     ap.add_argument("--n", type=int, default=256)
     ap.add_argument("--b", type=int, default=1024)
     ap.add_argument("--iters", type=int, default=10)
-    ap.add_argument("--mode", default="f32", choices=["f32", "f16"])
+    ap.add_argument("--mode", default="f32", choices=["f64", "f32", "f16"])
     ap.add_argument("--reps", type=int, default=3)
     args = ap.parse_args()
-    mode = PrecisionMode.EMULATED32 if args.mode == "f32" else PrecisionMode.F16
+    mode = {"f64": PrecisionMode.FULL64, "f32": PrecisionMode.EMULATED32, "f16": PrecisionMode.F16}[args.mode]
     a = spd_stack(args.n, args.b)
     sa = SplitStack.from_float(a)
     c = SplitStack(args.n, args.b, args.b)
