@@ -254,3 +254,19 @@ def test_ndb_chain_reads_upper_stored_input():
     _, zu, _ = roots.ndb_split(y1u, None, 0.0, 6, PrecisionMode.EMULATED32, complete=False)
     _, z, _ = roots.ndb_split(y1, None, 0.0, 6, PrecisionMode.EMULATED32)
     assert torch.equal(z.to_float(), roots.fill_lower(zu).to_float())
+
+
+@pytest.mark.parametrize("m,n,k", [(128, 256, 64), (37, 53, 29), (300, 700, 130), (256, 256, 1000), (1024, 1024, 1024),
+                                   (256, 128, 2048)])
+def test_bmm_full64_ring_vs_float64(m, n, k):
+    """FULL64 products accumulate in 16 K ranges per tile (ring mode: every range drained from TMEM into fp32
+    registers), including K ranges shorter than 16 k-blocks and a ragged last range: relF < 1e-6."""
+    torch.manual_seed(2)
+    a = torch.randn(3, m, k, device="cuda")
+    b = torch.randn(3, k, n, device="cuda")
+    c = linalg.bmm(a, b, PrecisionMode.FULL64)
+    c32 = linalg.bmm(a, b, PrecisionMode.EMULATED32)
+    ref = (a.double() @ b.double()).cpu().numpy()
+    e64, e32 = relf(c.cpu().numpy(), ref), relf(c32.cpu().numpy(), ref)
+    print(f"bmm K={k}: FULL64 {e64:.2e}  EMULATED32 {e32:.2e}")
+    assert e64 < 1e-6 and e64 <= e32 * 1.01
