@@ -14,7 +14,7 @@ import torch
 
 from .errors import NumericalError
 
-_LIB_PATH = Path(__file__).resolve().parent / "libdash_b200.so"
+_LIB_PATH = Path(os.environ.get("DASH_LIB") or Path(__file__).resolve().parent / "libdash_b200.so")  # DASH_LIB: A/B builds (dev)
 _lib: ctypes.CDLL | None = None
 
 DASH_OK, DASH_EINVAL, DASH_ENONFINITE, DASH_ECUDA = 0, 1, 2, 3

@@ -661,9 +661,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         // put every pass into slot c = K range c of nacc.
         if (ring) {  // ---- ring mode: units of per_u k-blocks, unit u -> slot u % kSl
           const int per_u = (nk + nring - 1) / nring;
+          uint32_t u = ucount;  // the current unit (counters, not divisions: this loop is issue-latency bound)
+          int kin = 0;          // k-blocks of the current unit issued
           for (int kb = 0; kb < nk; ++kb) {
-            const bool first = kb % per_u == 0;
-            const uint32_t u = ucount + static_cast<uint32_t>(kb / per_u);
+            const bool first = kin == 0;
             const uint32_t slot = u % kSl;
             if (first) {
               const long long w0 = prof ? clock64() : 0;
@@ -698,9 +699,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             }
             umma2_commit_mc_elect(&empty[stage]);
             if (++stage == C::kStages) { stage = 0; phase ^= 1; }
-            if (kb % per_u == per_u - 1 || kb == nk - 1) umma2_commit_mc_elect(&tfull[slot]);
+            if (++kin == per_u || kb == nk - 1) {
+              umma2_commit_mc_elect(&tfull[slot]);
+              ++u;
+              kin = 0;
+            }
           }
-          ucount += static_cast<uint32_t>((nk + per_u - 1) / per_u);
+          ucount = u;
           continue;
         }
         const int nmain = mc ? 1 : (mc4 ? 3 : nacc);
@@ -711,10 +716,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         constexpr uint32_t kSbo = KB == 64 ? 1024u : 512u, kLay = KB == 64 ? 2u : 4u;
         const uint32_t base = (t % nsets) * static_cast<uint32_t>(nacc);
         const uint32_t corr_slot = base + static_cast<uint32_t>(nacc - 1);
+        const uint32_t d_corr = tmem_base + corr_slot * kPN;
         const uint32_t use_par = ((t / nsets) & 1u) ^ 1u;
+        int c = 0, kin = 0;  // main slot and k-blocks issued into it (counters: no divisions in the issue loop)
         for (int kb = 0; kb < nk; ++kb) {
-          const bool first = kb % per == 0;
-          const uint32_t slot = base + static_cast<uint32_t>(kb / per);
+          const bool first = kin == 0;
+          const uint32_t slot = base + static_cast<uint32_t>(c);
           if (first || (corr && kb == 0)) {
             const long long w0 = prof ? clock64() : 0;
             if (first) mbar_wait(&tempty[slot], use_par);
@@ -751,16 +758,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
               // a slot's first write overwrites (main: pass 0 of its first k step; correction: pass 1 of k-block 0)
               const uint32_t fresh = to_corr ? ((kb == 0 && k == 0 && p == 1) ? 0u : 1u)
                                              : ((first && k == 0 && p == 0) ? 0u : 1u);
-              umma2_f16_elect(to_corr ? tmem_base + corr_slot * kPN : d_tmem, ad, bd, idesc, fresh);
+              umma2_f16_elect(to_corr ? d_corr : d_tmem, ad, bd, idesc, fresh);
             }
           }
           umma2_commit_mc_elect(&empty[stage]);
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
-          if (kb % per == per - 1 || kb == nk - 1) umma2_commit_mc_elect(&tfull[slot]);  // K range complete
+          if (++kin == per || kb == nk - 1) {  // this main slot's K range is complete
+            umma2_commit_mc_elect(&tfull[slot]);
+            ++c;
+            kin = 0;
+          }
           if (corr && kb == nk - 1) umma2_commit_mc_elect(&tfull[corr_slot]);
         }
         // main slots without k-blocks (nk < nmain): keep every slot's phase in step
-        for (int c = (nk + per - 1) / per; c < nmain; ++c) {
+        for (; c < nmain; ++c) {
           const uint32_t slot = base + static_cast<uint32_t>(c);
           mbar_wait(&tempty[slot], use_par);
           tc_fence_after();
