@@ -305,7 +305,7 @@ def bench_parity(iters: int, method: str = "ndb", precision: str = "f32") -> dic
 
     upd = max(relf(c - p, oc - op) for c, p, oc, op in zip(cur, prev, ocur, oprev))
     rts = max(relf(g.roots.double().cpu().numpy(), og["roots"]) for g, og in zip(st.groups, ost["groups"]))
-    tol = {"f32": (2e-3, 5e-3), "f16": (3e-2, 5e-2)}[precision]
+    tol = {"f32": (5e-4, 1e-4), "f16": (3e-2, 5e-2)}[precision]
     return {"case": f"layers {shapes}, B=1024, groups 1024/p4 x4 + 1024/p2 x1, 3 steps, last compared",
             "relF_update": upd, "relF_roots": rts, "tol": {"update": tol[0], "roots": tol[1]},
             "pass": bool(upd < tol[0] and rts < tol[1])}
@@ -452,10 +452,15 @@ def run_dash(args):
     peak = peaks.get("bf16_tflops_sustained", 1420.2)
     achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
     issued_tf = gemm_issued / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
-    traffic = None
-    tr_file = ROOT / "profiles" / "r1_gemm_traffic.json"
-    if tr_file.exists():
-        traffic = json.loads(tr_file.read_text()).get("bytes_per_launch")
+    # DRAM bytes per launch of the dominant launch (the Newton-DB Y*E / E*Z launch over the 1820-block group) from
+    # the committed ncu --set full capture of this build: ncu cannot run inside a timed bench (it replays kernels)
+    traffic, traffic_src = None, None
+    for name in ("r2_gemm_traffic.json", "r1_gemm_traffic.json"):
+        tr_file = ROOT / "profiles" / name
+        if tr_file.exists():
+            tr = json.loads(tr_file.read_text())
+            traffic, traffic_src = tr.get("bytes_per_launch"), f"profiles/{name}: {tr.get('source')}"
+            break
     result = {
         "metric": METRIC,
         "value": round(ms, 3),
@@ -496,6 +501,7 @@ def run_dash(args):
             "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4),
             "traffic": traffic,
+            "traffic_source": traffic_src,
             "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)",
             "flops_per_step": {k: round(v / 1e12, 3) for k, v in fl.items()},
             "gemm_launches_timed": n_gemm,

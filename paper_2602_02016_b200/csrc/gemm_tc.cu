@@ -115,8 +115,9 @@ __device__ __forceinline__ void store_split(__half* hi, long long plane, int ld,
 // 128 x 128 sub-block twice (direct and transposed) and drops the one below-diagonal sub-block of each
 // diagonal tile, so every output element has exactly one writer (deterministic).
 constexpr int kPairM = kTileM, kHalf = kTileM / 2;
-constexpr int kNaccDefault = 2;   // split-f16 accumulators per tile (env DASH_NACC = 1, 2 = main + correction,
-                                   // 4 = three K-range mains + correction, 8 / 16 = ring of that many K ranges)
+constexpr int kNaccDefault = 4;   // split-f16 accumulation (env DASH_NACC): 1 = one accumulator, 2 = main +
+                                   // correction, 4 / 8 / 16 = ring of that many K ranges per tile (4: the
+                                   // EMULATED32 default, as fast as 2 and ~4x more accurate; 16: FULL64)
 constexpr int kEpiWarps = 8;     // 2 per TMEM lane quarter, 64 columns each
 constexpr int kSlots = 4;         // TMEM accumulator slots (4 x 128 columns = all 512)
 constexpr int kRing = 8;          // tile-index ring shared by the pair (dynamic scheduling)
@@ -468,11 +469,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
   constexpr int kRounds = NT / 128;          // epilogue passes over a tile (128 columns each)
   constexpr uint32_t kSl = 512 / NT;         // TMEM slots
   const int nacc_req = NT == 128 ? (nacc_in & 0xff) : 1;
-  // ring mode (split products, nacc_req = R >= 8): the K loop of a tile is cut into R ranges ("units"); unit u of
+  // ring mode (split products, nacc_req = R >= 4): the K loop of a tile is cut into R ranges ("units"); unit u of
   // the launch accumulates in TMEM slot u % 4 and the epilogue adds it into registers (fp32, round to nearest)
   // and releases the slot, so each truncating tensor-core accumulation chain is K / R long while the four slots
   // keep the MMA running ahead of the epilogue
-  const bool ring = PASSES == 3 && nacc_req >= 8;
+  const bool ring = PASSES == 3 && nacc_req >= 4;
   const int nring = ring ? nacc_req : 0;
   const int nacc = ring ? static_cast<int>(kSl) : nacc_req;  // accumulators per tile (1, 2 or 4; 1 for NT = 256)
   const bool mc = PASSES == 3 && nacc == 2;  // main (hi*hi) + correction (hi*lo + lo*hi) accumulators

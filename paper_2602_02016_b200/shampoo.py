@@ -385,13 +385,21 @@ class _Runtime:
         if getattr(self, "chunks", None) and self.chunks_key == key:
             return self.chunks
         self.close_chunks()
-        total, target = sum(self.sizes), sum(self.sizes) / nchunks
-        bounds, acc = [0], 0
-        for i, sz in enumerate(self.sizes):
-            acc += sz
-            if acc >= target * len(bounds) and len(bounds) < nchunks and i + 1 < len(self.sizes):
+        # the first chunk's upload and the last chunk's download are the only copies nothing hides: make those
+        # chunks one layer each, and cut the layers between them into nchunks - 2 chunks of about equal size
+        nl = len(self.sizes)
+        lo, hi = (1, nl - 1) if nchunks >= 3 and nl >= 3 else (0, nl)
+        inner = max(1, nchunks - (2 if lo else 0))
+        target = sum(self.sizes[lo:hi]) / inner
+        bounds, acc = ([0, lo] if lo else [0]), 0
+        for i in range(lo, hi):
+            acc += self.sizes[i]
+            if acc >= target * (len(bounds) - (1 if lo else 0)) and len(bounds) < inner + (1 if lo else 0) \
+                    and i + 1 < hi:
                 bounds.append(i + 1)
-        bounds.append(len(self.sizes))
+        if hi < nl:
+            bounds.append(hi)
+        bounds.append(nl)
         chunks = []
         for c0, c1 in zip(bounds[:-1], bounds[1:]):
             owned = set()
@@ -410,7 +418,6 @@ class _Runtime:
                     ranges.append((gi, slots[0], slots[-1] + 1))
             chunks.append(_Chunk(c0, c1, int(self.offsets[c0]), int(self.offsets[c1]), plan, ws, blocks_c, ranges))
         self.chunks, self.chunks_key = chunks, key
-        del total
         return chunks
 
     def close_chunks(self) -> None:

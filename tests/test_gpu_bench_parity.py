@@ -7,7 +7,8 @@
   Newton and Chebyshev.  The GPU solves the whole 256-block stack; the oracle checks a sample of its blocks
   (every block is solved independently: results do not depend on the batch composition).
 
-Tolerances (relative Frobenius): split-f16 products with fp32 accumulation (EMULATED32), stated per test.
+Tolerances (relative Frobenius): split-f16 products with fp32 accumulation in 4 K ranges per tile (EMULATED32,
+the benchmark's mode), stated per test next to the measured values (profiles/r2_parity_ring4.log).
 """
 import numpy as np
 import pytest
@@ -51,8 +52,8 @@ def test_bench_config_multi_group_steps_vs_oracle():
     upd = max(relf(c - p, oc - op) for c, p, oc, op in zip(cur, prev, ocur, oprev))
     rts = [relf(g.roots.cpu().numpy(), og["roots"]) for g, og in zip(st.groups, ost["groups"])]
     print(f"bench-config last-step update relF {upd:.2e}, roots relF per group {[f'{r:.1e}' for r in rts]}")
-    assert upd < 2e-3
-    assert max(rts) < 5e-3
+    assert upd < 5e-4   # measured 1.5e-4 (ring accumulation R = 4)
+    assert max(rts) < 1e-4
 
 
 def _c2_stack(b, cond):
@@ -76,7 +77,7 @@ def test_c2_ndb_256_blocks_vs_oracle(b, cond):
     _, oz, _ = core.batched_newton_db(oy, 0.0, 10)
     errs = [relf(z[i], oz[k]) for k, i in enumerate(SAMPLE)]
     print(f"C2 NDB B={b} cond={cond:g}: {[f'{e:.1e}' for e in errs]}")
-    assert max(errs) < (2e-4 if cond <= 10 else 2e-3)
+    assert max(errs) < (3e-5 if cond <= 10 else 3e-4)  # measured <= 1.1e-5 / 1.3e-4 at B = 1024
 
 
 @pytest.mark.parametrize("b", [256, 512, 1024])
@@ -90,7 +91,7 @@ def test_c2_cn_256_blocks_vs_oracle(b, cond):
     ox, _ = core.batched_coupled_newton(a[SAMPLE], 4, 0.0, 10)
     errs = [relf(x[i], ox[k]) for k, i in enumerate(SAMPLE)]
     print(f"C2 CN B={b} cond={cond:g}: {[f'{e:.1e}' for e in errs]}")
-    assert max(errs) < (2e-4 if cond <= 10 else 2e-3)
+    assert max(errs) < (2e-5 if cond <= 10 else 1.5e-4)  # measured <= 5.6e-6 / 4.8e-5
 
 
 @pytest.mark.parametrize("b", [256, 512, 1024])
@@ -107,7 +108,7 @@ def test_c2_chebyshev_256_blocks_vs_oracle(b, cond):
     want = core.batched_clenshaw(a[SAMPLE], coeffs, scales[SAMPLE], 4)
     errs = [relf(out[i], want[k]) for k, i in enumerate(SAMPLE)]
     print(f"C2 Chebyshev B={b} cond={cond:g}: {[f'{e:.1e}' for e in errs]}")
-    assert max(errs) < 1e-3
+    assert max(errs) < (2e-5 if cond <= 10 else 8e-4)  # measured <= 6.6e-6 / 3.3e-4
 
 
 def _inv_sqrt(a):
@@ -115,11 +116,12 @@ def _inv_sqrt(a):
     return (q / np.sqrt(w)[..., None, :]) @ np.swapaxes(q, -1, -2)
 
 
-@pytest.mark.parametrize("mode,tol", [(PrecisionMode.FULL64, 1.5e-5), (PrecisionMode.EMULATED32, 2e-4)])
+@pytest.mark.parametrize("mode,tol", [(PrecisionMode.FULL64, 1.5e-5), (PrecisionMode.EMULATED32, 6e-5)])
 def test_ndb_accuracy_b1024_cond100_vs_eigh(mode, tol):
     """Converged Newton-DB (12 iterations) on B = 1024, cond 1e2 blocks against the float64 eigh inverse square
-    root: FULL64 accumulates each product in 16 K ranges (ring mode) and reaches the 1e-5 class; EMULATED32
-    (main + correction accumulators, the benchmark's mode) ~1.4e-4 (profiles/r2_ring.log)."""
+    root: FULL64 accumulates each product in 16 K ranges (ring mode) and reaches the 1e-5 class (1.02e-5);
+    EMULATED32 (4 K ranges, the benchmark's mode) 3.8e-5 (round 1's main + correction pair: 1.4e-4;
+    profiles/r2_ring_accumulation.log)."""
     a = np.stack([core.random_spd(1024, 1e2, seed=i, scale=0.5) for i in range(4)])
     _, z, _ = roots.batched_newton_db(torch.as_tensor(a, dtype=torch.float32, device="cuda"),
                                       roots.NdbConfig(tolerance=0.0, max_iters=12), mode)
