@@ -784,15 +784,18 @@ def _step_pipelined(state: ShampooState, params, grads, cfg: ShampooConfig, seed
     h2d.wait_stream(comp)
     out = torch.empty(rt.theta_out.numel(), dtype=torch.float32, pin_memory=True)
 
-    def upload(ch) -> torch.cuda.Event:
+    def upload(ch):
+        """Chunk ch's gradients, then its parameters (needed only by the apply): (grads event, params event)."""
+        evs = []
         with torch.cuda.stream(h2d):
-            for li in range(ch.l0, ch.l1):
-                o0, o1 = int(rt.offsets[li]), int(rt.offsets[li + 1])
-                rt.grad[o0:o1].copy_(grads[li].reshape(-1), non_blocking=True)
-                rt.theta[o0:o1].copy_(params[li].reshape(-1), non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(h2d)
-        return ev
+            for src, dst in ((grads, rt.grad), (params, rt.theta)):
+                for li in range(ch.l0, ch.l1):
+                    o0, o1 = int(rt.offsets[li]), int(rt.offsets[li + 1])
+                    dst[o0:o1].copy_(src[li].reshape(-1), non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(h2d)
+                evs.append(ev)
+        return evs
 
     # chunk k+1's copies are issued after chunk k's work is enqueued: the solvers' small job-table uploads then
     # never queue behind gigabytes of pending H2D traffic (the host would block on them)
@@ -806,7 +809,7 @@ def _step_pipelined(state: ShampooState, params, grads, cfg: ShampooConfig, seed
         events.setdefault("start", []).append(torch.cuda.Event(enable_timing=True))
         events["start"][-1].record()
     for k, ch in enumerate(chunks):
-        comp.wait_event(ev_next)
+        comp.wait_event(ev_next[0])
         _lib.check(L.dash_plan_accumulate(ch.plan, float(cfg.graft.beta2), float(cfg.graft.beta1), t + 1,
                                           float(cfg.graft.graft_eps), _lib.stream_ptr()), "dash_plan_accumulate")
         for gi, s0, e0 in ch.ranges:  # linalg.symmetrize + max|a| / sum(a^2) of the chunk's members
@@ -818,6 +821,7 @@ def _step_pipelined(state: ShampooState, params, grads, cfg: ShampooConfig, seed
             for gi, s0, e0 in ch.ranges:
                 _refresh_range(state, cfg, gi, s0, e0, step_seed, err, oks[k_ok:k_ok + 1])
                 k_ok += 1
+        comp.wait_event(ev_next[1])
         _lib.check(L.dash_plan_apply(ch.plan, rt.theta.data_ptr(), rt.theta_out.data_ptr(), eta, _lib.stream_ptr()),
                    "dash_plan_apply")
         if k + 1 < len(chunks):
