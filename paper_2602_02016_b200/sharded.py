@@ -173,7 +173,8 @@ class ShardedDash:
         refresh_inverse_roots(st, cfg, seed=block_seed(seed, t), defer_check=True)
         mark("refreshed")
         rt.load(rt.theta, params)
-        rt.theta_out.copy_(rt.theta)
+        # no theta_out <- theta copy: the apply writes every owned block and the unpack every other rank's, and the
+        # blocks partition the parameter space
         _lib.check(_lib.lib().dash_plan_apply(rt.plan, rt.theta.data_ptr(), rt.theta_out.data_ptr(),
                                               float(cfg.lr.value(t)), _lib.stream_ptr()), "dash_plan_apply")
         mark("applied")
