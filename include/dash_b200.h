@@ -110,9 +110,11 @@ int dash_cn(const dash_stack* a, const float* inv_scale, int p, float c, const d
             void* stream);
 /* dash_scale_stack: v = value * mult[m]^pw -> fp32 f_out and/or split dst (the root rescale
  *   roots * scales^(-1/p), shampoo.py:348, with mult = 1/scale and pw = 1/p).  gate (device int, may be
- *   NULL): nothing is written unless *gate != 0 (a group that failed its scale checks keeps its roots). */
+ *   NULL): nothing is written unless *gate != 0 (a group that failed its scale checks keeps its roots).
+ *   src_upper: src is in upper pair-block storage (dash_ndb_upper output); the lower blocks are read
+ *   transposed, so the outputs are complete without a dash_fill_lower pass. */
 int dash_scale_stack(const dash_stack* src, const float* mult, float pw, float* f_out, long long f_mat_stride,
-                     int f_ld, const dash_stack* dst, const int* gate, void* stream);
+                     int f_ld, const dash_stack* dst, const int* gate, int src_upper, void* stream);
 /* dash_scale_check: the refresh's scale checks for one group, on the device (shampoo.py:324-325,
  *   spectral.py:99-107): status[m] == 2 (pool collapsed twice) -> code 2 (DegenerateSpectrumError), a
  *   non-positive / non-finite scale[m] -> code 1 (ConvergenceError).  err[2] is shared by the groups of one

@@ -66,7 +66,8 @@ _SIGNATURES: dict[str, tuple] = {
     "dash_cn_ws_bytes": (c_size_t, [c_int, c_int]),
     "dash_cn": (c_int, [_P, c_void_p, c_int, c_float, _P, c_float, c_float, c_int, c_int, c_void_p, c_void_p,
                         c_void_p, c_void_p, c_size_t, c_void_p]),
-    "dash_scale_stack": (c_int, [_P, c_void_p, c_float, c_void_p, c_longlong, c_int, _P, c_void_p, c_void_p]),
+    "dash_scale_stack": (c_int, [_P, c_void_p, c_float, c_void_p, c_longlong, c_int, _P, c_void_p, c_int,
+                                 c_void_p]),
     "dash_scale_check": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
     "dash_cheb_ws_bytes": (c_size_t, [c_int, c_int]),
     "dash_clenshaw": (c_int, [_P, c_void_p, c_void_p, c_void_p, c_int, c_void_p, _P, c_int, c_void_p, c_void_p,

@@ -54,12 +54,13 @@ int dash_cn(const dash_stack* a, const float* inv_scale, int p, float c, const d
 }
 
 int dash_scale_stack(const dash_stack* src, const float* mult, float pw, float* f_out, long long f_mat_stride,
-                     int f_ld, const dash_stack* dst, const int* gate, void* stream) {
+                     int f_ld, const dash_stack* dst, const int* gate, int src_upper, void* stream) {
   if (!stack_ok(src) || (dst && !square_same(src, dst) && !(stack_ok(dst) && dst->rows == src->rows &&
                                                               dst->cols == src->cols && dst->nmat == src->nmat)))
     return DASH_EINVAL;
   if (!f_out && !dst) return DASH_EINVAL;
-  return scale_stack(*src, mult, pw, f_out, f_mat_stride, f_ld, dst, gate, static_cast<cudaStream_t>(stream));
+  return scale_stack(*src, mult, pw, f_out, f_mat_stride, f_ld, dst, gate, src_upper,
+                     static_cast<cudaStream_t>(stream));
 }
 
 int dash_scale_check(const float* scale, const int* status, int n, int group, int* ok, int* err, void* stream) {

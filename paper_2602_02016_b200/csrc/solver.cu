@@ -305,6 +305,59 @@ __global__ void scale_stack_kernel(dash_stack src, const float* __restrict__ mul
   }
 }
 
+// scale_stack of an upper pair-block stored source (the Newton-DB root as it leaves the solver): every 32 x 32
+// destination tile reads its source tile coalesced -- itself on / above the block diagonal, the transposed
+// upper tile below it -- through shared memory, so the completion pass (fill_lower) is fused away.
+__global__ void scale_stack_upper_kernel(dash_stack src, const float* __restrict__ mult, float pw,
+                                         float* __restrict__ f_out, long long f_mat_stride, int f_ld, dash_stack dst,
+                                         int has_dst, const int* __restrict__ gate) {
+  if (gate && *gate == 0) return;
+  __shared__ uint16_t th[32][33], tl[32][33];
+  const int m = blockIdx.z;
+  const int rows = src.rows, cols = src.cols;
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  const bool lower = (r0 >> 8) > (c0 >> 8);
+  const int sr0 = lower ? c0 : r0, sc0 = lower ? r0 : c0;
+  const float mu = mult ? (pw == 1.f ? mult[m] : static_cast<float>(pow(static_cast<double>(mult[m]), static_cast<double>(pw)))) : 1.f;
+  const float sc = ldexpf(1.f, src.exp[m]) * mu;
+  int e = 0;
+  const float bound = __uint_as_float(src.amax[m]) * fabsf(mu);
+  if (bound > 0.f && bound < 3.0e38f) { frexpf(bound, &e); e -= 15; }
+  const float inv = ldexpf(1.f, -e);
+  const uint16_t* sh = reinterpret_cast<const uint16_t*>(mat_hi(src, m));
+  const long long sp = mat_plane(src);
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int r = sr0 + i, c = sc0 + static_cast<int>(threadIdx.x);
+    const bool in = r < rows && c < cols;
+    th[i][threadIdx.x] = in ? sh[static_cast<long long>(r) * src.ld + c] : 0;
+    tl[i][threadIdx.x] = in ? sh[sp + static_cast<long long>(r) * src.ld + c] : 0;
+  }
+  __syncthreads();
+  __half* dh = has_dst ? mat_hi(dst, m) : nullptr;
+  const long long dp = has_dst ? mat_plane(dst) : 0;
+  float amax = 0.f;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int r = r0 + i, c = c0 + static_cast<int>(threadIdx.x);
+    if (r >= rows) continue;
+    const uint16_t hb = lower ? th[threadIdx.x][i] : th[i][threadIdx.x];
+    const uint16_t lb = lower ? tl[threadIdx.x][i] : tl[i][threadIdx.x];
+    const float v = (c < cols) ? (__half2float(__ushort_as_half(hb)) + __half2float(__ushort_as_half(lb))) * sc : 0.f;
+    if (f_out && c < cols) f_out[m * f_mat_stride + static_cast<long long>(r) * f_ld + c] = v;
+    if (has_dst && c < dst.ld) {
+      const float y = v * inv;
+      const __half h = __float2half_rn(y);
+      dh[static_cast<long long>(r) * dst.ld + c] = h;
+      dh[dp + static_cast<long long>(r) * dst.ld + c] = __float2half_rn(y - __half2float(h));
+      amax = nonneg_max(amax, fabsf(v));
+    }
+  }
+  if (has_dst) {
+    amax = warp_max_nonneg(amax);
+    if ((threadIdx.x & 31) == 0) atomic_max_nonneg(dst.amax + m, amax);
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && threadIdx.y == 0) dst.exp[m] = e;
+  }
+}
+
 static dim3 egrid(const dash_stack& s) {
   long long el = static_cast<long long>(s.rows) * s.cols;
   long long b = (el + 255) / 256;
@@ -315,13 +368,19 @@ static dim3 egrid(const dash_stack& s) {
 static int cuda_ok() { return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_ECUDA; }
 
 int scale_stack(const dash_stack& src, const float* mult, float pw, float* f_out, long long f_mat_stride, int f_ld,
-                const dash_stack* dst, const int* gate, cudaStream_t st) {
+                const dash_stack* dst, const int* gate, int src_upper, cudaStream_t st) {
   dash_stack d{};
   if (dst) {
     d = *dst;
     zero_amax(gate, d.nmat, d.amax, nullptr, nullptr, st);
   }
-  scale_stack_kernel<<<egrid(src), 256, 0, st>>>(src, mult, pw, f_out, f_mat_stride, f_ld, d, dst ? 1 : 0, gate);
+  if (src_upper && ndb_upper_storage()) {
+    const dim3 grid((src.ld + 31) / 32, (src.rows + 31) / 32, src.nmat);
+    scale_stack_upper_kernel<<<grid, dim3(32, 8), 0, st>>>(src, mult, pw, f_out, f_mat_stride, f_ld, d, dst ? 1 : 0,
+                                                           gate);
+  } else {
+    scale_stack_kernel<<<egrid(src), 256, 0, st>>>(src, mult, pw, f_out, f_mat_stride, f_ld, d, dst ? 1 : 0, gate);
+  }
   note_launch();
   return cuda_ok();
 }

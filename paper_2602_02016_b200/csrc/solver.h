@@ -21,7 +21,7 @@ int cheb_solve(const dash_stack& a, const float* inv_scale, const float* mult, c
                float* f_out, const dash_stack* out_split, int passes, const int* gate, void* ws, size_t ws_bytes,
                cudaStream_t st);
 int scale_stack(const dash_stack& src, const float* mult, float pw, float* f_out, long long f_mat_stride, int f_ld,
-                const dash_stack* dst, const int* gate, cudaStream_t st);
+                const dash_stack* dst, const int* gate, int src_upper, cudaStream_t st);
 int scale_check(const float* scale, const int* status, int n, int group, int* ok, int* err, cudaStream_t st);
 
 }  // namespace dash

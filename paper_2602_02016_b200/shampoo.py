@@ -33,7 +33,7 @@ from .eigensolver import DampeningHeuristic, HeuristicKind, evd_inverse_root_tor
 from .errors import ConvergenceError, DegenerateSpectrumError
 from .linalg import (PrecisionMode, Scratch, SplitStack, device, format_matrix, parse_matrix, passes_for, stall_for,
                      workspace)
-from .roots import CnConfig, DeviceReports, IterationReport, cn_split, fill_lower, ndb_split
+from .roots import CnConfig, DeviceReports, IterationReport, cn_split, ndb_split
 from .spectral import Frobenius, PowerIterationScaling, ScalingMode, block_seed, power_iteration_scales
 
 SOLVER_METHODS = ("evd", "cn", "ndb", "cbshv")
@@ -635,8 +635,6 @@ def _refresh_range(state: ShampooState, cfg: ShampooConfig, gi: int, s: int, e: 
         _, src, r2 = ndb_split(y1, None, solver.tolerance, solver.max_iters, mode, complete=False, scratch=sc,
                                tag="ndb2")
         reps = [r1, r2]
-    if solver.method == "ndb":
-        fill_lower(src)
     fallback = None
     if tol_mode:  # per-block reports, in the reference's order (first chain, then second)
         lists = [r.to_list() for r in reps]
@@ -654,8 +652,10 @@ def _refresh_range(state: ShampooState, cfg: ShampooConfig, gi: int, s: int, e: 
         for lst in lists:
             _check_reports(group, lst, offset=s)
     # roots = Z * scale^(-1/p)  -> fp32 state roots + split copy for the apply (gated on the scale checks)
+    # (the Newton-DB root is still in upper pair-block storage: the rescale reads its lower blocks transposed)
     _lib.check(L.dash_scale_stack(src.ref(), inv.data_ptr(), 1.0 / p, roots.data_ptr(), roots.stride(0),
-                                  roots.stride(1), rsplit.ref(), ok.data_ptr(), _lib.stream_ptr()), "dash_scale_stack")
+                                  roots.stride(1), rsplit.ref(), ok.data_ptr(), int(solver.method == "ndb"),
+                                  _lib.stream_ptr()), "dash_scale_stack")
     if fallback:
         idx = torch.tensor(fallback, dtype=torch.long, device=rt.dev)
         roots[idx] = inverse_root_f64(ema[idx], cfg.epsilon, p)

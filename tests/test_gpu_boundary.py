@@ -250,3 +250,28 @@ def test_pipelined_host_step_bitwise_equals_device_step(method):
         assert torch.equal(a.cpu(), b)
     for ga, gb in zip(st_d.groups, st_h.groups):
         assert torch.equal(ga.roots, gb.roots) and torch.equal(ga.ema, gb.ema)
+
+
+def test_partition_device_bitexact_and_split_operand_bound():
+    """blocking.partition (blocking.py:84-98) on a CUDA tensor == on NumPy, bit for bit; the step's in-place
+    block operand (grad_split_kernel: hi + lo fp16 planes with a per-block power-of-two exponent) reproduces
+    every gradient block to within 2^-21 of the block's max |g| per element (the a2 contract)."""
+    from paper_2602_02016_b200.blocking import partition
+
+    rng = np.random.default_rng(9)
+    g = rng.standard_normal((300, 200)) * np.geomspace(1e-6, 1.0, 200)[None, :]
+    pn = partition(g, 64)
+    pt = partition(torch.as_tensor(g, device="cuda"), 64)
+    assert np.array_equal(pt.full_blocks.cpu().numpy(), pn.full_blocks)
+    for (s1, b1), (s2, b2) in zip(pt.blocks(), pn.blocks()):
+        assert s1 == s2 and np.array_equal(b1.cpu().numpy(), b2)
+    cfg = shampoo.ShampooConfig(block_size=64, solver=shampoo.SolverConfig(tolerance=0.0, max_iters=2))
+    st = shampoo.init_state([g.astype(np.float32)], cfg)
+    shampoo.accumulate(st, [g.astype(np.float32)], cfg)
+    torch.cuda.synchronize()
+    ops = st.runtime.gsm.to_float().double().cpu().numpy()
+    g32 = g.astype(np.float32).astype(np.float64)
+    for i, ((r0, r1), (c0, c1)) in enumerate(st.layers[0].layout.block_spans):
+        blk = g32[r0:r1, c0:c1]
+        err = np.abs(ops[i, : r1 - r0, : c1 - c0] - blk).max()
+        assert err <= 2.0 ** -21 * np.abs(blk).max(), (i, err)

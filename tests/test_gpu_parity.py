@@ -270,3 +270,29 @@ def test_bmm_full64_ring_vs_float64(m, n, k):
     e64, e32 = relf(c.cpu().numpy(), ref), relf(c32.cpu().numpy(), ref)
     print(f"bmm K={k}: FULL64 {e64:.2e}  EMULATED32 {e32:.2e}")
     assert e64 < 1e-6 and e64 <= e32 * 1.01
+
+
+@pytest.mark.parametrize("b", [640, 1024])
+def test_scale_stack_reads_upper_storage(b):
+    """dash_scale_stack on the upper pair-block stored Newton-DB root (src_upper = 1) == dash_fill_lower followed by
+    the plain rescale, bit for bit, for the fp32 roots and their split copy (the refresh's fused completion)."""
+    from paper_2602_02016_b200 import _lib
+    from paper_2602_02016_b200.linalg import SplitStack
+
+    a = np.stack([core.random_spd(b, c, seed=50 + i, scale=0.5) for i, c in enumerate([10.0, 1e2, 1e3])])
+    sa = SplitStack.from_float(torch.tensor(a, dtype=torch.float32, device="cuda"))
+    _, zu, _ = roots.ndb_split(sa, None, 0.0, 6, PrecisionMode.EMULATED32, complete=False)
+    mult = torch.tensor([0.5, 2.0, 0.25], device="cuda")
+    L, s = _lib.lib(), _lib.stream_ptr()
+    outs = []
+    for upper in (1, 0):
+        if not upper:
+            roots.fill_lower(zu)
+        f = torch.zeros(3, b, b, device="cuda")
+        d = SplitStack(3, b, b)
+        _lib.check(L.dash_scale_stack(zu.ref(), mult.data_ptr(), 0.25, f.data_ptr(), f.stride(0), f.stride(1), d.ref(),
+                                      None, upper, s), "dash_scale_stack")
+        outs.append((f, d))
+    (f1, d1), (f0, d0) = outs
+    assert torch.equal(f1, f0)
+    assert torch.equal(d1.data, d0.data) and torch.equal(d1.exp, d0.exp) and torch.equal(d1.amax, d0.amax)
