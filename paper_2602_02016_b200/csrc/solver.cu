@@ -305,56 +305,78 @@ __global__ void scale_stack_kernel(dash_stack src, const float* __restrict__ mul
   }
 }
 
-// scale_stack of an upper pair-block stored source (the Newton-DB root as it leaves the solver): every 32 x 32
-// destination tile reads its source tile coalesced -- itself on / above the block diagonal, the transposed
-// upper tile below it -- through shared memory, so the completion pass (fill_lower) is fused away.
-__global__ void scale_stack_upper_kernel(dash_stack src, const float* __restrict__ mult, float pw,
-                                         float* __restrict__ f_out, long long f_mat_stride, int f_ld, dash_stack dst,
-                                         int has_dst, const int* __restrict__ gate) {
+// scale_stack of an upper pair-block stored source (the Newton-DB root as it leaves the solver): every 64 x 64
+// destination tile stages its source tile in shared memory with 16-byte loads -- the tile itself on / above the
+// block diagonal, the transposed upper tile below it -- so the completion pass (fill_lower) is fused away; the
+// outputs are written as 8-column vectors like scale_stack_kernel, with the same arithmetic (bit-identical).
+constexpr int kSuT = 64, kSuPad = 8;  // tile edge; padding of the staged rows (halves)
+__global__ void __launch_bounds__(256) scale_stack_upper_kernel(dash_stack src, const float* __restrict__ mult,
+                                                                float pw, float* __restrict__ f_out,
+                                                                long long f_mat_stride, int f_ld, dash_stack dst,
+                                                                int has_dst, const int* __restrict__ gate) {
   if (gate && *gate == 0) return;
-  __shared__ uint16_t th[32][33], tl[32][33];
+  __shared__ __align__(16) __half th[kSuT][kSuT + kSuPad], tl[kSuT][kSuT + kSuPad];
   const int m = blockIdx.z;
   const int rows = src.rows, cols = src.cols;
-  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  const int r0 = blockIdx.y * kSuT, c0 = blockIdx.x * kSuT;
   const bool lower = (r0 >> 8) > (c0 >> 8);
-  const int sr0 = lower ? c0 : r0, sc0 = lower ? r0 : c0;
+  const int sr0 = lower ? c0 : r0, sc0 = lower ? r0 : c0;  // source tile (upper storage)
   const float mu = mult ? (pw == 1.f ? mult[m] : static_cast<float>(pow(static_cast<double>(mult[m]), static_cast<double>(pw)))) : 1.f;
   const float sc = ldexpf(1.f, src.exp[m]) * mu;
   int e = 0;
   const float bound = __uint_as_float(src.amax[m]) * fabsf(mu);
   if (bound > 0.f && bound < 3.0e38f) { frexpf(bound, &e); e -= 15; }
   const float inv = ldexpf(1.f, -e);
-  const uint16_t* sh = reinterpret_cast<const uint16_t*>(mat_hi(src, m));
+  const __half* sh = mat_hi(src, m);
   const long long sp = mat_plane(src);
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int r = sr0 + i, c = sc0 + static_cast<int>(threadIdx.x);
-    const bool in = r < rows && c < cols;
-    th[i][threadIdx.x] = in ? sh[static_cast<long long>(r) * src.ld + c] : 0;
-    tl[i][threadIdx.x] = in ? sh[sp + static_cast<long long>(r) * src.ld + c] : 0;
+  // stage: 64 rows x 8 chunks of 8 halves per plane; src.ld is a multiple of 64, so chunks never straddle a row
+  for (int t = threadIdx.x; t < kSuT * (kSuT / 8); t += blockDim.x) {
+    const int i = t >> 3, c8 = (t & 7) * 8;
+    const int r = sr0 + i;
+    uint4 h = make_uint4(0, 0, 0, 0), l = h;
+    if (r < rows && sc0 + c8 < src.ld) {
+      const long long off = static_cast<long long>(r) * src.ld + sc0 + c8;
+      h = __ldg(reinterpret_cast<const uint4*>(sh + off));
+      l = __ldg(reinterpret_cast<const uint4*>(sh + sp + off));
+    }
+    *reinterpret_cast<uint4*>(&th[i][c8]) = h;
+    *reinterpret_cast<uint4*>(&tl[i][c8]) = l;
   }
   __syncthreads();
   __half* dh = has_dst ? mat_hi(dst, m) : nullptr;
   const long long dp = has_dst ? mat_plane(dst) : 0;
   float amax = 0.f;
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int r = r0 + i, c = c0 + static_cast<int>(threadIdx.x);
-    if (r >= rows) continue;
-    const uint16_t hb = lower ? th[threadIdx.x][i] : th[i][threadIdx.x];
-    const uint16_t lb = lower ? tl[threadIdx.x][i] : tl[i][threadIdx.x];
-    const float v = (c < cols) ? (__half2float(__ushort_as_half(hb)) + __half2float(__ushort_as_half(lb))) * sc : 0.f;
-    if (f_out && c < cols) f_out[m * f_mat_stride + static_cast<long long>(r) * f_ld + c] = v;
+  for (int t = threadIdx.x; t < kSuT * (kSuT / 8); t += blockDim.x) {
+    const int i = t >> 3, c8 = (t & 7) * 8;
+    const int r = r0 + i, c = c0 + c8;
+    if (r >= rows || c >= (has_dst ? dst.ld : cols)) continue;  // (padding columns of dst are written as zeros)
+    float v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const __half h = lower ? th[c8 + k][i] : th[i][c8 + k];
+      const __half l = lower ? tl[c8 + k][i] : tl[i][c8 + k];
+      v[k] = (c + k < cols) ? (__half2float(h) + __half2float(l)) * sc : 0.f;
+    }
+    if (f_out) {
+      float* fo = f_out + m * f_mat_stride + static_cast<long long>(r) * f_ld + c;
+      if (c + 8 <= cols && (f_ld & 3) == 0 && ((m * f_mat_stride) & 3) == 0) {
+        reinterpret_cast<float4*>(fo)[0] = make_float4(v[0], v[1], v[2], v[3]);
+        reinterpret_cast<float4*>(fo)[1] = make_float4(v[4], v[5], v[6], v[7]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) if (c + k < cols) fo[k] = v[k];
+      }
+    }
     if (has_dst && c < dst.ld) {
-      const float y = v * inv;
-      const __half h = __float2half_rn(y);
-      dh[static_cast<long long>(r) * dst.ld + c] = h;
-      dh[dp + static_cast<long long>(r) * dst.ld + c] = __float2half_rn(y - __half2float(h));
-      amax = nonneg_max(amax, fabsf(v));
+      store_split8(dh, dp, static_cast<long long>(r) * dst.ld + c, v, inv);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) amax = nonneg_max(amax, fabsf(v[k]));
     }
   }
   if (has_dst) {
     amax = warp_max_nonneg(amax);
     if ((threadIdx.x & 31) == 0) atomic_max_nonneg(dst.amax + m, amax);
-    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && threadIdx.y == 0) dst.exp[m] = e;
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) dst.exp[m] = e;
   }
 }
 
@@ -375,9 +397,8 @@ int scale_stack(const dash_stack& src, const float* mult, float pw, float* f_out
     zero_amax(gate, d.nmat, d.amax, nullptr, nullptr, st);
   }
   if (src_upper && ndb_upper_storage()) {
-    const dim3 grid((src.ld + 31) / 32, (src.rows + 31) / 32, src.nmat);
-    scale_stack_upper_kernel<<<grid, dim3(32, 8), 0, st>>>(src, mult, pw, f_out, f_mat_stride, f_ld, d, dst ? 1 : 0,
-                                                           gate);
+    const dim3 grid((src.ld + kSuT - 1) / kSuT, (src.rows + kSuT - 1) / kSuT, src.nmat);
+    scale_stack_upper_kernel<<<grid, 256, 0, st>>>(src, mult, pw, f_out, f_mat_stride, f_ld, d, dst ? 1 : 0, gate);
   } else {
     scale_stack_kernel<<<egrid(src), 256, 0, st>>>(src, mult, pw, f_out, f_mat_stride, f_ld, d, dst ? 1 : 0, gate);
   }
