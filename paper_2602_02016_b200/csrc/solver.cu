@@ -91,8 +91,11 @@ __device__ bool watch_push(float* h, int* hl, float r) {
 // stall > 0 (a tolerance below the precision floor, see SolverConfig): a block whose residual stops decreasing
 // (r_k >= r_{k-1}) once r_{k-1} <= stall has reached the rounding floor of the arithmetic and is frozen as
 // converged there (checked after the non-finite and tolerance rules, before the watch).
+// z0..z2 (nullable): amax arrays of the next iteration's GEMM outputs, zeroed here when blocks stay active (the
+// gated GEMMs refill them), which saves two launches per Newton-DB iteration.
 __global__ void freeze_kernel(BlockState s, int n, int k, float tol, float stall, int first, int* iters,
-                              float* resid_out, int* conv, int* newly_frozen) {
+                              float* resid_out, int* conv, int* newly_frozen, unsigned* z0 = nullptr,
+                              unsigned* z1 = nullptr, unsigned* z2 = nullptr) {
   __shared__ int cnt;
   if (threadIdx.x == 0) {
     cnt = 0;
@@ -133,6 +136,12 @@ __global__ void freeze_kernel(BlockState s, int n, int k, float tol, float stall
   atomicAdd(&cnt, local);
   __syncthreads();
   if (threadIdx.x == 0) *s.n_active = cnt;
+  if (cnt > 0)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      if (z0) z0[i] = 0u;
+      if (z1) z1[i] = 0u;
+      if (z2) z2[i] = 0u;
+    }
 }
 
 // Reports of blocks still active after the loop: (max_iters, last residual, False) (roots.py:302-304).
@@ -592,18 +601,22 @@ int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_o
   note_launch();
   if (int rc = g_first.run(passes, st)) return rc;
   ++np;
-  freeze_kernel<<<1, 1024, 0, st>>>(s, n, 1, tol, stall, 1, iters, resid_out, conv, nullptr);
+  // each freeze also zeroes the amax arrays the next iteration's (gated) GEMMs fill: E and the Y / Z pair of
+  // parity par ^ 1 (iteration k reads (Y, Z)[par] and writes (Y, Z)[par ^ 1])
+  freeze_kernel<<<1, 1024, 0, st>>>(s, n, 1, tol, stall, 1, iters, resid_out, conv, nullptr, e.amax,
+                                    ys[0].amax, zs[0].amax);
   note_launch();
   set_par_kernel<<<1, 1, 0, st>>>(s.par, 1);  // Y1, Z1 live in the scratch pair
   int par = 1;
   note_launch();
   for (int k = 2; k <= max_iters; ++k) {
-    zero_amax(s.n_active, n, e.amax, nullptr, nullptr, st);
     if (int rc = g_e[par].run(passes, st, s.n_active)) return rc;
-    zero_amax(s.n_active, n, ys[par ^ 1].amax, zs[par ^ 1].amax, nullptr, st);
     if (int rc = g_yz[par].run(passes, st, s.n_active)) return rc;
     np += 3;
-    freeze_kernel<<<1, 1024, 0, st>>>(s, n, k, tol, stall, 0, iters, resid_out, conv, nullptr);
+    const bool more = k < max_iters;  // the next iteration writes (Y, Z)[par] (par flips below)
+    freeze_kernel<<<1, 1024, 0, st>>>(s, n, k, tol, stall, 0, iters, resid_out, conv, nullptr,
+                                      more ? e.amax : nullptr, more ? ys[par].amax : nullptr,
+                                      more ? zs[par].amax : nullptr);
     note_launch();
     par ^= 1;
   }
