@@ -275,7 +275,10 @@ int job_tiles(const GemmJob& j, int nt) {
 
 void JobBuilder::push(GemmJob& j) {
   static const int no_sym = getenv("DASH_NO_SYM") ? atoi(getenv("DASH_NO_SYM")) : 0;  // diagnostic knob
-  if (j.sym && (no_sym || j.M != j.N || j.op == EPI_EMA || j.op == EPI_APPLY)) j.sym = 0;
+  // symmetric jobs: solver products (split outputs, mirrored as split tiles) and the statistics EMA (fp32 in / out,
+  // mirrored through the transposed fp32 map; needs the TMA-staged fp32 path)
+  if (j.sym && (no_sym || j.M != j.N || j.op == EPI_APPLY || (j.op == EPI_EMA && (j.f_map < 0 || j.f_tmap < 0))))
+    j.sym = 0;
   // TMA-staged split stores need the job to cover its output matrix exactly (padding stays zero)
   static const int no_tma = getenv("DASH_NO_TMA_STORE") ? atoi(getenv("DASH_NO_TMA_STORE")) : 0;
   if (no_tma || !j.c_hi || j.M != j.c_rows || j.N != j.c_cols || j.c_map < 0 || j.c_tmap < 0 ||

@@ -787,6 +787,9 @@ dash_plan* dash_plan_create(const dash_block* blocks, int nb_m, int nb_v, int bl
       const int d = p->gdim[k.group_l];
       js.set_fout(j, p->gema[k.group_l], p->gsize[k.group_l], d, d, k.slot_l, true);
     }
+    // G G^T (and G^T G, g g^T) is symmetric: only the tiles on / above the diagonal run, the epilogue writes the
+    // transposed tile below (the EMA input of a lower tile is the transpose of its upper one)
+    j.sym = j.f_map >= 0 ? 1 : 0;
     js.push(j);
     if (mat) {  // R
       if (!js.operands(j, gs, sidx, 1, gs, sidx, 0, false)) { delete p; return fail(DASH_EINVAL); }
@@ -795,6 +798,7 @@ dash_plan* dash_plan_create(const dash_block* blocks, int nb_m, int nb_v, int bl
       j.beta = beta_lr;
       const int d = p->gdim[k.group_r];
       js.set_fout(j, p->gema[k.group_r], p->gsize[k.group_r], d, d, k.slot_r, true);
+      j.sym = j.f_map >= 0 ? 1 : 0;
       js.push(j);
     }
     // ---- apply jobs
