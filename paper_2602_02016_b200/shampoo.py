@@ -530,9 +530,10 @@ def check_step_status(state: ShampooState) -> None:
     if err is None:
         return
     rt.pending_err = None
-    vals = err.tolist()
-    if vals[0]:
-        _raise_scale_error(state, vals)
+    vals = err.tolist()  # one (code, group) pair per refresh stream: the reference raises for the first group
+    fails = [vals[i:i + 2] for i in range(0, len(vals), 2) if vals[i]]
+    if fails:
+        _raise_scale_error(state, min(fails, key=lambda f: f[1]))
 
 
 def refresh_inverse_roots(state: ShampooState, cfg: ShampooConfig, seed: int = 0, *, defer_check: bool = False
@@ -554,14 +555,35 @@ def refresh_inverse_roots(state: ShampooState, cfg: ShampooConfig, seed: int = 0
         _group_stats(state, cfg)
     rt.stats_valid = True
     err, oks = _refresh_flags(rt, len(state.groups))
-    for gi, group in enumerate(state.groups):
-        if cfg.solver.method == "evd":
+    if cfg.solver.method == "evd":
+        for gi, group in enumerate(state.groups):
             group.roots.copy_(evd_inverse_root_torch(group.ema, group.exponent, cfg.solver.heuristic))
             rt.root_split[gi].load(group.roots)
-            continue
-        _refresh_range(state, cfg, gi, 0, len(group.members), seed, err, oks[gi:gi + 1])
+        return state
+    # Fixed-iteration refreshes run the groups other than the largest on a second stream with their own scratch
+    # and error word: their short, few-wave launches fill the big group's launch tails instead of running alone.
+    # Every per-block computation is stream- and batch-independent, so the roots are bit-identical.
+    side = len(state.groups) > 1 and not cfg.solver.require_convergence
+    big = max(range(len(state.groups)), key=lambda g: len(state.groups[g].members) * state.groups[g].dim ** 3)
+    main = torch.cuda.current_stream()
+    if side:
+        if getattr(rt, "side_stream", None) is None:
+            rt.side_stream, rt.side_scratch = torch.cuda.Stream(device=rt.dev), Scratch(rt.dev)
+        rt.side_stream.wait_stream(main)
+        err_side = rt.side_scratch.tensor("err", (2,), torch.int32)
+        with torch.cuda.stream(rt.side_stream):
+            err_side.zero_()
+    for gi, group in enumerate(state.groups):
+        if side and gi != big:
+            with torch.cuda.stream(rt.side_stream):
+                _refresh_range(state, cfg, gi, 0, len(group.members), seed, err_side, oks[gi:gi + 1],
+                               scratch=rt.side_scratch)
+        else:
+            _refresh_range(state, cfg, gi, 0, len(group.members), seed, err, oks[gi:gi + 1])
+    if side:
+        main.wait_stream(rt.side_stream)
     if not cfg.solver.require_convergence:
-        rt.pending_err = err
+        rt.pending_err = torch.cat([err, err_side]) if side else err
         if not defer_check:
             check_step_status(state)
     return state
@@ -575,14 +597,14 @@ def _refresh_flags(rt: "_Runtime", nflags: int):
 
 
 def _refresh_range(state: ShampooState, cfg: ShampooConfig, gi: int, s: int, e: int, seed: int,
-                   err: torch.Tensor, ok: torch.Tensor) -> None:
+                   err: torch.Tensor, ok: torch.Tensor, scratch: Scratch | None = None) -> None:
     """Scale, solve, check and commit the roots of group `gi`'s members [s, e) (the whole group, or one chunk of
     the pipelined host step); every per-block computation is independent of the range, so any partition of a
     group gives bit-identical roots."""
     rt: _Runtime = state.runtime
     solver = cfg.solver
     L = _lib.lib()
-    sc = rt.scratch
+    sc = scratch if scratch is not None else rt.scratch
     group = state.groups[gi]
     p, n, d = group.exponent, e - s, group.dim
     gids = getattr(rt, "global_gid", None)  # block sharding: rank-local group gi is global group gids[gi]
