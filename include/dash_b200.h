@@ -144,6 +144,11 @@ dash_plan* dash_plan_create(const dash_block* blocks, int nb_m, int nb_v, int bl
                             uint32_t* gamax, float* graft_s, float beta_lr, int passes, void* ws, size_t ws_bytes,
                             void* stream, int* status);
 void dash_plan_destroy(dash_plan* p);
+/* Owner-only optimizer state (block sharding; PAPER.md:114 keeps each block's Adam / momentum on its owner):
+ * d_offsets (device, nb_m + nb_v entries, multiples of 4, caller-owned, must outlive the plan's use) gives each
+ * block's base in a packed adam / mom buffer holding the blocks back to back (row-major inside a block).
+ * NULL (the default) indexes adam / mom like the flat parameter space. */
+int dash_plan_set_state_offsets(dash_plan* p, const long long* d_offsets);
 int dash_plan_un_stride(const dash_plan* p);
 int dash_prep_parts(void);
 /* Length of each block's slice of the apply-norm partial buffer (`un_part`) for a given block size. */

@@ -78,6 +78,7 @@ _SIGNATURES: dict[str, tuple] = {
                                     c_void_p, c_void_p, c_void_p, c_float, c_int, c_void_p, c_size_t, c_void_p,
                                     ctypes.POINTER(c_int)]),
     "dash_plan_destroy": (None, [c_void_p]),
+    "dash_plan_set_state_offsets": (c_int, [c_void_p, c_void_p]),
     "dash_plan_un_stride": (c_int, [c_void_p]),
     "dash_prep_parts": (c_int, []),
     "dash_apply_partials": (c_int, [c_int]),

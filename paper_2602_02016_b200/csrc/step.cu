@@ -52,23 +52,27 @@ __device__ double block_sum_d(double v, double* sh) {
 __global__ void __launch_bounds__(256) prep_kernel(const dash_block* __restrict__ blocks, const float* __restrict__ g,
                                                    float* __restrict__ adam, float* __restrict__ mom, float beta2,
                                                    float beta1, float bc1_inv, float bc2_inv, float geps,
-                                                   float* __restrict__ pn_part, unsigned* __restrict__ gamax) {
+                                                   float* __restrict__ pn_part, unsigned* __restrict__ gamax,
+                                                   const long long* __restrict__ sofs) {
   __shared__ double sh[8];
   const int b = blockIdx.y, p = blockIdx.x;
   const dash_block blk = blocks[b];
+  // optimizer state index of block element e: the flat parameter index (sofs == NULL) or, for an owner-only
+  // state (block sharding), the block's packed base + e (block-major, row-major inside the block)
+  const long long sb = sofs ? sofs[b] : -1;
   const long long total = static_cast<long long>(blk.rows) * blk.cols;
   const long long per = (total + kPrepParts - 1) / kPrepParts;
   const long long e0 = p * per, e1 = min(total, e0 + per);
   double pn = 0.0;
   float mx = 0.f;
-  auto one = [&](long long i) {
+  auto one = [&](long long i, long long si) {
     const float gv = g[i];
-    const float a = beta2 * adam[i] + (1.f - beta2) * gv * gv;
-    adam[i] = a;
+    const float a = beta2 * adam[si] + (1.f - beta2) * gv * gv;
+    adam[si] = a;
     float num = gv;
     if (mom) {
-      const float m = beta1 * mom[i] + (1.f - beta1) * gv;
-      mom[i] = m;
+      const float m = beta1 * mom[si] + (1.f - beta1) * gv;
+      mom[si] = m;
       num = m * bc1_inv;
     }
     const float pv = num / (geps + sqrtf(a * bc2_inv));
@@ -80,24 +84,25 @@ __global__ void __launch_bounds__(256) prep_kernel(const dash_block* __restrict_
   // rows of 4-aligned 4-multiple width (every 2-D block and 1-D chunk of the DASH shapes): 16-byte accesses
   const bool contiguous = blk.ld == blk.cols || blk.rows == 1;
   const long long w = contiguous ? total : blk.cols;  // elements per contiguous run
-  if (w % 4 == 0 && blk.off % 4 == 0 && blk.ld % 4 == 0 && (e0 % 4 == 0) && (per % 4 == 0)) {
+  if (w % 4 == 0 && blk.off % 4 == 0 && blk.ld % 4 == 0 && (e0 % 4 == 0) && (per % 4 == 0) && (sb < 0 || sb % 4 == 0)) {
     for (long long e = e0 + 4 * threadIdx.x; e < e1; e += 4 * blockDim.x) {
       const long long r = contiguous ? 0 : e / blk.cols, c = contiguous ? e : e % blk.cols;
       const long long i = blk.off + r * blk.ld + c;
+      const long long si = sb < 0 ? i : sb + e;
       const float4 g4 = *reinterpret_cast<const float4*>(g + i);
-      float4 a4 = *reinterpret_cast<const float4*>(adam + i);
+      float4 a4 = *reinterpret_cast<const float4*>(adam + si);
       const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
       float av4[4] = {a4.x, a4.y, a4.z, a4.w};
       float num[4] = {gv[0], gv[1], gv[2], gv[3]};
       if (mom) {
-        float4 m4 = *reinterpret_cast<const float4*>(mom + i);
+        float4 m4 = *reinterpret_cast<const float4*>(mom + si);
         float mv[4] = {m4.x, m4.y, m4.z, m4.w};
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           mv[k] = beta1 * mv[k] + (1.f - beta1) * gv[k];
           num[k] = mv[k] * bc1_inv;
         }
-        *reinterpret_cast<float4*>(mom + i) = make_float4(mv[0], mv[1], mv[2], mv[3]);
+        *reinterpret_cast<float4*>(mom + si) = make_float4(mv[0], mv[1], mv[2], mv[3]);
       }
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -108,12 +113,13 @@ __global__ void __launch_bounds__(256) prep_kernel(const dash_block* __restrict_
         if (!(aa <= 3.0e38f)) aa = __uint_as_float(0x7fc00000u);
         mx = nonneg_max(mx, aa);
       }
-      *reinterpret_cast<float4*>(adam + i) = make_float4(av4[0], av4[1], av4[2], av4[3]);
+      *reinterpret_cast<float4*>(adam + si) = make_float4(av4[0], av4[1], av4[2], av4[3]);
     }
   } else {
     for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
       const int r = static_cast<int>(e / blk.cols), c = static_cast<int>(e % blk.cols);
-      one(blk.off + static_cast<long long>(r) * blk.ld + c);
+      const long long i = blk.off + static_cast<long long>(r) * blk.ld + c;
+      one(i, sb < 0 ? i : sb + e);
     }
   }
   const double t = block_sum_d<256>(pn, sh);
@@ -692,6 +698,7 @@ struct dash_plan {
   float *grad = nullptr, *adam = nullptr, *mom = nullptr, *um = nullptr, *uv = nullptr;
   float *pn_part = nullptr, *un_part = nullptr, *graft_s = nullptr;
   unsigned* gamax = nullptr;
+  const long long* sofs = nullptr;  // owner-only optimizer state: per-block packed offsets (device, caller-owned)
   int un_stride = 0;
   dash_stack gsm{}, gsv{}, tm{};
   dash::UploadedGemm g_stats, g_apply1, g_apply2;
@@ -842,6 +849,12 @@ dash_plan* dash_plan_create(const dash_block* blocks, int nb_m, int nb_v, int bl
 
 void dash_plan_destroy(dash_plan* p) { delete p; }
 
+int dash_plan_set_state_offsets(dash_plan* p, const long long* d_offsets) {
+  if (!p) return DASH_EINVAL;
+  p->sofs = d_offsets;
+  return DASH_OK;
+}
+
 // accumulate (shampoo.py:238-278) + graft-direction norms for step index t (n_acc = t + 1).
 int dash_plan_accumulate(dash_plan* p, float beta2, float beta1, int n_acc, float graft_eps, void* stream) {
   if (!p) return DASH_EINVAL;
@@ -851,7 +864,7 @@ int dash_plan_accumulate(dash_plan* p, float beta2, float beta1, int n_acc, floa
   const float bc2_inv = static_cast<float>(1.0 / (1.0 - std::pow(static_cast<double>(beta2), n_acc)));
   cudaMemsetAsync(p->gamax, 0, sizeof(unsigned) * nb, st);
   prep_kernel<<<dim3(kPrepParts, nb), 256, 0, st>>>(p->dblocks, p->grad, p->adam, p->mom, beta2, beta1, bc1_inv,
-                                                   bc2_inv, graft_eps, p->pn_part, p->gamax);
+                                                   bc2_inv, graft_eps, p->pn_part, p->gamax, p->sofs);
   note_launch();
   if (p->nb_m) {
     grad_split_kernel<<<dim3(32, p->nb_m), 256, 0, st>>>(p->dblocks, p->grad, p->gsm, p->gamax);

@@ -275,6 +275,16 @@ def block_rows(layers: list[LayerState], offsets, owned=None, slot_of=None):
     return mats, vecs
 
 
+def block_keys(layers: list[LayerState], owned=None) -> list[tuple[int, int]]:
+    """(layer_id, block_idx) of every block_rows row, in the same order (matrix blocks first, then chunks)."""
+    mats, vecs = [], []
+    for layer in layers:
+        n = len(layer.layout.block_spans) if layer.is_matrix else len(layer.chunk_bounds)
+        keys = [(layer.layer_id, i) for i in range(n) if owned is None or (layer.layer_id, i) in owned]
+        (mats if layer.is_matrix else vecs).extend(keys)
+    return mats + vecs
+
+
 @dataclass
 class _Chunk:
     """One pipeline chunk of the host-buffer step: layers [l0, l1) = flat elements [e0, e1)."""
@@ -287,6 +297,7 @@ class _Chunk:
     ws: torch.Tensor
     blocks_c: Any
     ranges: list  # (group index, first slot, end slot)
+    sofs: Any = None  # owner-only state: the chunk's blocks' packed state offsets (kept alive for the plan)
 
 
 class _Runtime:
@@ -301,13 +312,23 @@ class _Runtime:
         total = int(self.offsets[-1])
         f32 = dict(dtype=torch.float32, device=self.dev)
         self.grad = torch.zeros(total, **f32)
-        self.adam = torch.zeros(total, **f32)
-        self.mom = torch.zeros(total, **f32) if momentum else None
         self.theta = torch.zeros(total, **f32)
         self.theta_out = torch.zeros(total, **f32)
         mats, vecs = block_rows(state.layers, self.offsets, owned, slot_of)
         self.nb_m, self.nb_v = len(mats), len(vecs)
         nb = self.nb_m + self.nb_v
+        # Adam / momentum: over the flat parameter space, or -- for a rank's shard -- owner-only, the owned
+        # blocks packed back to back (each padded to a multiple of 4 elements for 16-byte access)
+        self.owned, self.slot_of = owned, slot_of
+        self.sofs, self.sofs_of = None, None
+        if owned is not None:
+            sizes = [(r[2] * r[3] + 3) // 4 * 4 for r in mats + vecs]
+            base = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+            self.sofs = torch.tensor(base[:-1], dtype=torch.int64, device=self.dev)
+            self.sofs_of = dict(zip(block_keys(state.layers, owned), base[:-1].tolist()))
+            total = int(base[-1])
+        self.adam = torch.zeros(total, **f32)
+        self.mom = torch.zeros(total, **f32) if momentum else None
         self.block_rows = mats + vecs
         Arr = _lib.dash_block * nb
         self.blocks_c = Arr(*[_lib.dash_block(*b) for b in self.block_rows])
@@ -348,8 +369,9 @@ class _Runtime:
     def views(self, flat: torch.Tensor) -> list[torch.Tensor]:
         return [flat[int(self.offsets[i]):int(self.offsets[i + 1])].view(s) for i, s in enumerate(self.shapes)]
 
-    def _create_plan(self, blocks_c, nb_m: int, nb_v: int, key):
-        """A C-ABI plan over a block table (all blocks, or one pipeline chunk's); returns (plan, workspace)."""
+    def _create_plan(self, blocks_c, nb_m: int, nb_v: int, key, sofs=None):
+        """A C-ABI plan over a block table (all blocks, or one pipeline chunk's); returns (plan, workspace).
+        `sofs`: the blocks' packed optimizer-state offsets (owner-only state), default this runtime's."""
         L = _lib.lib()
         ng = len(self.groups)
         gdim = (ctypes_int * ng)(*[g.dim for g in self.groups])
@@ -367,6 +389,9 @@ class _Runtime:
             key[1], ws.data_ptr(), ws.numel(), _lib.stream_ptr(), ctypes_byref(status))
         if not p:
             _lib.check(status.value or _lib.DASH_EINVAL, "dash_plan_create")
+        sofs = self.sofs if sofs is None else sofs
+        if sofs is not None:
+            _lib.check(L.dash_plan_set_state_offsets(p, sofs.data_ptr()), "dash_plan_set_state_offsets")
         return p, ws
 
     def ensure_plan(self, cfg: ShampooConfig) -> None:
@@ -377,18 +402,12 @@ class _Runtime:
         self.plan, self.plan_ws = self._create_plan(self.blocks_c, self.nb_m, self.nb_v, key)
         self.plan_key = key
 
-    def ensure_chunks(self, cfg: ShampooConfig, layers: list[LayerState], nchunks: int) -> list:
-        """Pipeline chunks of the host-buffer step: contiguous layer ranges of about equal size, each with its
-        own plan over its blocks and, per group, the contiguous slot range of its members (members are sorted
-        by layer, shampoo.py:185-202)."""
-        key = (cfg.beta_lr, passes_for(cfg.solver.precision), nchunks)
-        if getattr(self, "chunks", None) and self.chunks_key == key:
-            return self.chunks
-        self.close_chunks()
-        # the first chunk's upload and the last chunk's download are the only copies nothing hides: make those
-        # chunks one layer each, and cut the layers between them into nchunks - 2 chunks of about equal size
+    def chunk_bounds(self, nchunks: int, edges: bool = True) -> list[int]:
+        """Layer boundaries of `nchunks` contiguous chunks of about equal size.  `edges` (host-buffer step):
+        the first chunk's upload and the last chunk's download are the only copies nothing hides, so those
+        chunks are one layer each and the layers between them are cut into nchunks - 2 chunks."""
         nl = len(self.sizes)
-        lo, hi = (1, nl - 1) if nchunks >= 3 and nl >= 3 else (0, nl)
+        lo, hi = (1, nl - 1) if edges and nchunks >= 3 and nl >= 3 else (0, nl)
         inner = max(1, nchunks - (2 if lo else 0))
         target = sum(self.sizes[lo:hi]) / inner
         bounds, acc = ([0, lo] if lo else [0]), 0
@@ -400,23 +419,43 @@ class _Runtime:
         if hi < nl:
             bounds.append(hi)
         bounds.append(nl)
+        return bounds
+
+    def ensure_chunks(self, cfg: ShampooConfig, layers: list[LayerState], nchunks: int, edges: bool = True) -> list:
+        """Pipeline chunks of the host-buffer step (or of a rank's overlapped exchange): contiguous layer ranges
+        of about equal size, each with its own plan over its (owned) blocks and, per group, the contiguous slot
+        range of its members (members are sorted by layer, shampoo.py:185-202)."""
+        key = (cfg.beta_lr, passes_for(cfg.solver.precision), nchunks, edges)
+        if getattr(self, "chunks", None) and self.chunks_key == key:
+            return self.chunks
+        self.close_chunks()
+        bounds = self.chunk_bounds(nchunks, edges)
         chunks = []
         for c0, c1 in zip(bounds[:-1], bounds[1:]):
             owned = set()
             for lay in layers[c0:c1]:
                 nb = len(lay.layout.block_spans) if lay.is_matrix else len(lay.chunk_bounds)
-                owned.update((lay.layer_id, i) for i in range(nb))
-            mats, vecs = block_rows(layers, self.offsets, owned)
+                owned.update((lay.layer_id, i) for i in range(nb)
+                             if self.owned is None or (lay.layer_id, i) in self.owned)
+            if not owned:  # (a rank's shard may hold no block of a layer range)
+                chunks.append(_Chunk(c0, c1, int(self.offsets[c0]), int(self.offsets[c1]), None, None, None, []))
+                continue
+            mats, vecs = block_rows(layers, self.offsets, owned, self.slot_of)
             rows = mats + vecs
             blocks_c = (_lib.dash_block * len(rows))(*[_lib.dash_block(*b) for b in rows])
-            plan, ws = self._create_plan(blocks_c, len(mats), len(vecs), key)
+            sofs = None
+            if self.sofs_of is not None:
+                sofs = torch.tensor([self.sofs_of[k] for k in block_keys(layers, owned)], dtype=torch.int64,
+                                    device=self.dev)
+            plan, ws = self._create_plan(blocks_c, len(mats), len(vecs), key, sofs)
             ranges = []
             for gi, g in enumerate(self.groups):
                 slots = [k for k, m in enumerate(g.members) if c0 <= m[0] < c1]
                 if slots:
                     assert slots == list(range(slots[0], slots[-1] + 1))
                     ranges.append((gi, slots[0], slots[-1] + 1))
-            chunks.append(_Chunk(c0, c1, int(self.offsets[c0]), int(self.offsets[c1]), plan, ws, blocks_c, ranges))
+            chunks.append(_Chunk(c0, c1, int(self.offsets[c0]), int(self.offsets[c1]), plan, ws, blocks_c, ranges,
+                                 sofs))
         self.chunks, self.chunks_key = chunks, key
         return chunks
 
@@ -784,6 +823,22 @@ def _pipelined(state: ShampooState, params, grads, cfg: ShampooConfig) -> bool:
             and len(params) == len(rt.shapes) and len(grads) == len(rt.shapes) and pinned(params) and pinned(grads))
 
 
+def accumulate_chunk(state: ShampooState, cfg: ShampooConfig, ch: _Chunk, t: int) -> None:
+    """accumulate() restricted to one chunk's blocks (its plan indexes the split gradients, graft partials and
+    block maxima by chunk-local block, so a chunk's apply must follow its own accumulate)."""
+    rt: _Runtime = state.runtime
+    L = _lib.lib()
+    if ch.plan is None:
+        return
+    _lib.check(L.dash_plan_accumulate(ch.plan, float(cfg.graft.beta2), float(cfg.graft.beta1), t + 1,
+                                      float(cfg.graft.graft_eps), _lib.stream_ptr()), "dash_plan_accumulate")
+    for gi, s0, e0 in ch.ranges:  # linalg.symmetrize + max|a| / sum(a^2) of the chunk's members
+        g = state.groups[gi]
+        _lib.check(L.dash_group_sym(g.ema[s0:e0].data_ptr(), e0 - s0, g.dim, float(cfg.epsilon),
+                                    rt.g_amax[gi][s0:e0].data_ptr(), rt.g_fro[gi][s0 * rt.prep_parts:].data_ptr(),
+                                    _lib.stream_ptr()), "dash_group_sym")
+
+
 def _step_pipelined(state: ShampooState, params, grads, cfg: ShampooConfig, seed: int, events: dict | None):
     """shampoo.step for host buffers: layer chunk k's gradients and parameters go up, its statistics, roots and
     update are computed, and its new parameters come down while chunk k+1 is transferred and computed
@@ -832,13 +887,7 @@ def _step_pipelined(state: ShampooState, params, grads, cfg: ShampooConfig, seed
         events["start"][-1].record()
     for k, ch in enumerate(chunks):
         comp.wait_event(ev_next[0])
-        _lib.check(L.dash_plan_accumulate(ch.plan, float(cfg.graft.beta2), float(cfg.graft.beta1), t + 1,
-                                          float(cfg.graft.graft_eps), _lib.stream_ptr()), "dash_plan_accumulate")
-        for gi, s0, e0 in ch.ranges:  # linalg.symmetrize + max|a| / sum(a^2) of the chunk's members
-            g = state.groups[gi]
-            _lib.check(L.dash_group_sym(g.ema[s0:e0].data_ptr(), e0 - s0, g.dim, float(cfg.epsilon),
-                                        rt.g_amax[gi][s0:e0].data_ptr(), rt.g_fro[gi][s0 * rt.prep_parts:].data_ptr(),
-                                        _lib.stream_ptr()), "dash_group_sym")
+        accumulate_chunk(state, cfg, ch, t)
         if refresh:
             for gi, s0, e0 in ch.ranges:
                 _refresh_range(state, cfg, gi, s0, e0, step_seed, err, oks[k_ok:k_ok + 1])

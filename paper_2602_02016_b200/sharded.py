@@ -22,8 +22,9 @@ import torch
 
 from . import _lib
 from .balance import block_balance, block_cost
-from .shampoo import (GroupSpec, LayerState, PrecondGroup, ShampooConfig, ShampooState, SlotRef, _Runtime,
-                      accumulate, block_rows, build_layout, check_step_status, refresh_inverse_roots)
+from .shampoo import (GroupSpec, LayerState, PrecondGroup, ShampooConfig, ShampooState, SlotRef, _refresh_flags,
+                      _refresh_range, _Runtime, accumulate, accumulate_chunk, block_rows, build_layout,
+                      check_step_status, refresh_inverse_roots)
 from .spectral import block_seed
 
 
@@ -102,7 +103,8 @@ class ShardedDash:
     another rank owns), so ``save_state`` refuses it rather than writing a partial checkpoint.
     """
 
-    def __init__(self, params, cfg: ShampooConfig, rank: int, world: int, group=None):
+    def __init__(self, params, cfg: ShampooConfig, rank: int, world: int, group=None,
+                 exchange_chunks: int | None = None):
         import torch.distributed as dist
 
         self.cfg, self.rank, self.world, self.group = cfg, rank, world, group
@@ -132,24 +134,33 @@ class ShardedDash:
         for lgi, sp in enumerate(lspecs):  # global slot of every local member (power-iteration seeds)
             gslot = {m: i for i, m in enumerate(specs[self.global_group_ids[lgi]].members)}
             rt.seed_index.append(torch.tensor([gslot[m] for m in sp.members], dtype=torch.int32, device=dev))
-        self.state.adam = rt.views(rt.adam)
-        self.state.momentum = rt.views(rt.mom) if rt.mom is not None else None
-        # exchange layout: rank q's blocks packed block-major (matrix blocks, then chunks) in order
-        sizes = [int(packed_positions(self.units, a)[-1]) for a in self.assignment]
-        self.max_packed = max(sizes)
-        self.allgather_bytes = 4 * self.max_packed * world
-        self.send = torch.zeros(self.max_packed, dtype=torch.float32, device=dev)
-        self.recv = torch.zeros(world * self.max_packed, dtype=torch.float32, device=dev)
+        # owner-only Adam / momentum: rt.adam / rt.mom hold this rank's blocks packed (rt.sofs), no per-layer views
+        self.state.adam = []
+        self.state.momentum = None
+        # exchange layout: per exchange chunk (a contiguous layer range), rank q's blocks of it packed block-major
+        # (matrix blocks, then chunks) in order; one all-gather per chunk
+        self.nx = exchange_chunks if exchange_chunks is not None else _exchange_chunks()
+        self.bounds = rt.chunk_bounds(self.nx, edges=False)
         self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.tables = []
-        for q in range(world):
-            ow = {(self.units[i].layer_id, self.units[i].idx) for i in self.assignment[q]}
-            m, v = block_rows(layers, rt.offsets, ow, slot_of={k: SlotRef(0, 0) for k in _all_keys(layers)})
-            rows = [r[:4] + (0, 0, -1, -1) for r in m + v]
-            blocks = _to_block_tensor(rows, dev)
-            pos = torch.tensor(packed_positions(self.units, self.assignment[q])[:-1] + q * self.max_packed,
-                               dtype=torch.int64, device=dev)
-            self.tables.append((blocks, pos, len(rows)))
+        any_slot = {k: SlotRef(0, 0) for k in _all_keys(layers)}
+        self.xchunks = []
+        for c0, c1 in zip(self.bounds[:-1], self.bounds[1:]):
+            parts = [[i for i in a if c0 <= self.units[i].layer_id < c1] for a in self.assignment]
+            mx = max(max(int(packed_positions(self.units, a)[-1]) for a in parts), 1)
+            tables = []
+            for q in range(world):
+                ow = {(self.units[i].layer_id, self.units[i].idx) for i in parts[q]}
+                m, v = block_rows(layers, rt.offsets, ow, slot_of=any_slot)
+                rows = [r[:4] + (0, 0, -1, -1) for r in m + v]
+                pos = torch.tensor(packed_positions(self.units, parts[q])[:-1] + q * mx, dtype=torch.int64,
+                                   device=dev)
+                tables.append((_to_block_tensor(rows, dev), pos, len(rows)))
+            self.xchunks.append(_XChunk(torch.zeros(mx, dtype=torch.float32, device=dev),
+                                        torch.zeros(world * mx, dtype=torch.float32, device=dev), mx, tables,
+                                        tables[rank][1] - rank * mx))
+        self.max_packed = sum(x.mx for x in self.xchunks)
+        self.allgather_bytes = 4 * self.max_packed * world
+        self.comm = torch.cuda.Stream(device=dev)
 
     @property
     def backend(self) -> str:
@@ -182,22 +193,107 @@ class ShardedDash:
         st.step = t + 1
         return rt.theta_out
 
-    def _all_gather(self) -> None:
-        if self.backend == "nccl":
-            self.dist.all_gather_into_tensor(self.recv, self.send, group=self.group)
-            return
-        host = torch.empty(self.world * self.max_packed, dtype=torch.float32)  # gloo: stage through the host
-        self.dist.all_gather_into_tensor(host, self.send.cpu(), group=self.group)
-        self.recv.copy_(host)
+    def _overlappable(self) -> bool:
+        """Fixed-iteration Newton / Chebyshev refreshes never raise on the host mid-step (their errors are one
+        device word read at the end), so their chunks can be computed between the exchange collectives."""
+        return self.nx > 1 and not self.cfg.solver.require_convergence and self.cfg.solver.method != "evd"
+
+    def _step_chunked(self, params, grads, seed: int, mark) -> None:
+        """step_local with the refresh and apply cut into the exchange chunks: chunk k's all-gather (comm
+        stream) runs under chunk k+1's solves.  Per-block work is independent of the chunking, so the result is
+        bit-identical to step_local's."""
+        st, cfg, rt = self.state, self.cfg, self.state.runtime
+        t = st.step
+        mark("start")
+        if len(grads) != len(st.layers):
+            raise ValueError(f"expected {len(st.layers)} gradients, got {len(grads)}")
+        for layer, g in zip(st.layers, grads):
+            if tuple(g.shape) != layer.shape:
+                raise ValueError(f"layer {layer.layer_id}: gradient shape {tuple(g.shape)} != {layer.shape}")
+        chunks = rt.ensure_chunks(cfg, st.layers, self.nx, edges=False)
+        rt.load(rt.grad, grads)
+        rt.load(rt.theta, params)
+        refresh = t % cfg.update_freq == 0
+        err, oks = _refresh_flags(rt, max(1, sum(len(ch.ranges) for ch in chunks)))
+        step_seed, eta, k_ok = block_seed(seed, t), float(cfg.lr.value(t)), 0
+        L = _lib.lib()
+        for k, ch in enumerate(chunks):
+            # the chunk plans share the split-gradient / graft scratch (indexed by chunk-local block), so a
+            # chunk's accumulate, refresh and apply run back to back
+            accumulate_chunk(st, cfg, ch, t)
+            if k == 0:
+                mark("accumulated")
+            if refresh:
+                for gi, s0, e0 in ch.ranges:
+                    _refresh_range(st, cfg, gi, s0, e0, step_seed, err, oks[k_ok:k_ok + 1])
+                    k_ok += 1
+            if k == len(chunks) - 1:
+                mark("refreshed")
+            if ch.plan is not None:
+                _lib.check(L.dash_plan_apply(ch.plan, rt.theta.data_ptr(), rt.theta_out.data_ptr(), eta,
+                                             _lib.stream_ptr()), "dash_plan_apply")
+            yield k
+        mark("applied")
+        rt.stats_valid, rt.stats_eps = True, cfg.epsilon
+        if refresh:
+            rt.pending_err = err
+        check_step_status(st)
+        st.step = t + 1
+
+    def _send(self, k: int) -> None:
+        """Pack this rank's blocks of exchange chunk k (after the compute stream's work so far) and start the
+        chunk's all-gather on the comm stream (NCCL) or run it host-staged (gloo)."""
+        x = self.xchunks[k]
+        rt = self.state.runtime
+        ready = torch.cuda.Event()
+        ready.record()
+        self.comm.wait_event(ready)
+        blocks, _, n = x.tables[self.rank]
+        with torch.cuda.stream(self.comm):
+            if n:
+                _lib.check(_lib.lib().dash_pack_blocks(blocks.data_ptr(), n, x.local_pos.data_ptr(),
+                                                       rt.theta_out.data_ptr(), x.send.data_ptr(),
+                                                       _lib.stream_ptr()), "dash_pack_blocks")
+            if self.backend == "nccl":
+                x.work = self.dist.all_gather_into_tensor(x.recv, x.send, group=self.group, async_op=True)
+            else:
+                host = torch.empty(self.world * x.mx, dtype=torch.float32)
+                self.dist.all_gather_into_tensor(host, x.send.cpu(), group=self.group)
+                x.recv.copy_(host)
+                x.work = None
 
     def step(self, params, grads, seed: int = 0, events: dict | None = None):
-        """One sharded DASH step; `params` (CUDA tensors) are updated in place on every rank."""
+        """One sharded DASH step; `params` (CUDA tensors) are updated in place on every rank.
+
+        Every rank issues the same collectives whatever happens locally: one all-gather per exchange chunk,
+        then an all-reduce of a failure flag; a rank that raised keeps sending (its data is never unpacked) so
+        no rank is left waiting, and every rank raises before touching `params` if any rank failed."""
         rt = self.state.runtime
+
+        def mark(name):
+            if events is not None:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record()
+                events.setdefault(name, []).append(ev)
+
         failure = None
+        sent = 0
         try:
-            self.step_local(params, grads, seed, events)
+            if self._overlappable():
+                for k in self._step_chunked(params, grads, seed, mark):
+                    self._send(k)
+                    sent = k + 1
+            else:
+                self.step_local(params, grads, seed, events)
         except Exception as exc:  # noqa: BLE001 - re-raised after the ranks agree
             failure = exc
+        for k in range(sent, len(self.xchunks)):
+            self._send(k)
+        torch.cuda.current_stream().wait_stream(self.comm)
+        for x in self.xchunks:
+            if x.work is not None:
+                x.work.wait()
+                x.work = None
         self.flag.fill_(1 if failure is not None else 0)
         if self.backend == "nccl":
             self.dist.all_reduce(self.flag, op=self.dist.ReduceOp.MAX, group=self.group)
@@ -209,26 +305,42 @@ class ShardedDash:
         if failure is not None:
             raise failure
         if bad:
-            raise RuntimeError("DASH step failed on another rank (see its error); no parameters were exchanged")
+            raise RuntimeError("DASH step failed on another rank (see its error); parameters left unchanged")
         L = _lib.lib()
-        blocks, pos, n = self.tables[self.rank]
-        local_pos = pos - self.rank * self.max_packed
-        _lib.check(L.dash_pack_blocks(blocks.data_ptr(), n, local_pos.data_ptr(), rt.theta_out.data_ptr(),
-                                      self.send.data_ptr(), _lib.stream_ptr()), "dash_pack_blocks")
-        self._all_gather()
-        for q in range(self.world):
-            if q == self.rank:
-                continue
-            b, p, nq = self.tables[q]
-            _lib.check(L.dash_unpack_blocks(b.data_ptr(), nq, p.data_ptr(), self.recv.data_ptr(),
-                                            rt.theta_out.data_ptr(), _lib.stream_ptr()), "dash_unpack_blocks")
+        for x in self.xchunks:
+            for q in range(self.world):
+                b, p, nq = x.tables[q]
+                if q == self.rank or not nq:
+                    continue
+                _lib.check(L.dash_unpack_blocks(b.data_ptr(), nq, p.data_ptr(), x.recv.data_ptr(),
+                                                rt.theta_out.data_ptr(), _lib.stream_ptr()), "dash_unpack_blocks")
         for p_, o in zip(params, rt.views(rt.theta_out)):
             p_.copy_(o)
-        if events is not None:
-            ev = torch.cuda.Event(enable_timing=True)
-            ev.record()
-            events.setdefault("exchanged", []).append(ev)
+        mark("exchanged")
         return params
+
+
+@dataclass
+class _XChunk:
+    """One exchange chunk: this rank's send buffer, the gathered buffer (world x mx), per-rank pack tables."""
+
+    send: torch.Tensor
+    recv: torch.Tensor
+    mx: int
+    tables: list
+    local_pos: torch.Tensor  # this rank's packed positions inside `send`
+    work: object = None
+
+
+def _exchange_chunks() -> int:
+    """Exchange chunks per step (env DASH_XCHUNKS, default 2): each chunk's all-gather hides under the next
+    chunk's solves; 1 = one all-gather after the whole step."""
+    import os
+
+    try:
+        return max(1, int(os.environ.get("DASH_XCHUNKS", "2")))
+    except ValueError:
+        return 2
 
 
 def _local_layer(lay: LayerState, slot_of) -> LayerState:

@@ -152,7 +152,15 @@ def test_two_shards_equal_unsharded_step_bitwise():
     assert torch.equal(merged, ref_flat)
 
 
-def _sharded_worker(rank, world, port, q):
+def _world2_cfg(nx):
+    """nx = 3 also carries graft momentum (owner-only packed momentum next to the packed Adam state)."""
+    from paper_2602_02016_b200.shampoo import GraftConfig, ShampooConfig, SolverConfig
+
+    return ShampooConfig(block_size=32, solver=SolverConfig(tolerance=0.0, max_iters=10),
+                         graft=GraftConfig(beta1=0.9 if nx == 3 else 0.0))
+
+
+def _sharded_worker(rank, world, port, q, nx=2):
     """One rank of a world-2 ShardedDash: the full step (accumulate, refresh, apply, C-ABI pack, all-gather,
     unpack) on cuda:0 over gloo (host-staged exchange), three steps, then the flat parameters go back."""
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -166,8 +174,10 @@ def _sharded_worker(rank, world, port, q):
     params = [torch.tensor(rng.standard_normal(s), dtype=torch.float32, device="cuda") for s in shapes]
     grads = [[torch.tensor(rng.standard_normal(s), dtype=torch.float32, device="cuda") for s in shapes]
              for _ in range(3)]
-    cfg = ShampooConfig(block_size=32, solver=SolverConfig(tolerance=0.0, max_iters=10))
-    opt = ShardedDash(params, cfg, rank=rank, world=world)
+    cfg = _world2_cfg(nx)
+    opt = ShardedDash(params, cfg, rank=rank, world=world, exchange_chunks=nx)
+    total = sum(int(np.prod(s)) for s in shapes)
+    assert opt.state.runtime.adam.numel() < total  # owner-only Adam state
     events = {}
     for gs in grads:
         opt.step(params, gs, seed=5, events=events)
@@ -177,8 +187,10 @@ def _sharded_worker(rank, world, port, q):
 
 
 @pytest.mark.gpu
-def test_sharded_step_world2_equals_single_gpu_bitwise():
-    """ShardedDash.step end to end on 2 ranks == the 1-GPU step, bit for bit, on both ranks."""
+@pytest.mark.parametrize("nx", [1, 2, 3])
+def test_sharded_step_world2_equals_single_gpu_bitwise(nx):
+    """ShardedDash.step end to end on 2 ranks == the 1-GPU step, bit for bit, on both ranks:
+    one all-gather after the step (nx = 1) or nx exchange chunks overlapped with the next chunk's solves."""
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
     from paper_2602_02016_b200.shampoo import ShampooConfig, SolverConfig, init_state, step
@@ -188,7 +200,7 @@ def test_sharded_step_world2_equals_single_gpu_bitwise():
     params = [torch.tensor(rng.standard_normal(s), dtype=torch.float32, device="cuda") for s in shapes]
     grads = [[torch.tensor(rng.standard_normal(s), dtype=torch.float32, device="cuda") for s in shapes]
              for _ in range(3)]
-    cfg = ShampooConfig(block_size=32, solver=SolverConfig(tolerance=0.0, max_iters=10))
+    cfg = _world2_cfg(nx)
     st = init_state(params, cfg)
     cur = [p.clone() for p in params]
     for gs in grads:
@@ -197,7 +209,7 @@ def test_sharded_step_world2_equals_single_gpu_bitwise():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q, nx)) for r in range(2)]
     for p in procs:
         p.start()
     res = {r: (flat, nex) for r, flat, nex in (q.get(timeout=300) for _ in procs)}
