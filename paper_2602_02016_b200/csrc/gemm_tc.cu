@@ -297,6 +297,37 @@ __device__ __forceinline__ void epi_piece(const GemmJob& jb, EpiCtx& cx, int c0,
     case EPI_CHEB:
     case EPI_CHEB_FINAL: {
       const bool fin = cx.op == EPI_CHEB_FINAL;
+      if (!fin && cx.sbuf && cx.row_ok && c0 + W <= cx.N) {
+        // full piece, staged side input: paired conversions, fused 2 (x sc) - s (exact scalings, one rounding,
+        // the same value as the general path), the diagonal term only where the diagonal crosses the piece
+        const float ss = cx.side_scale, s2 = 2.f * cx.sc;
+#pragma unroll
+        for (int c8 = 0; c8 < W / 8; ++c8) {
+          const int ch = (c0 - cx.lc0) / 8 + c8;
+          const int off = cx.lane * 128 + ((ch ^ (cx.lane & 7)) << 4);
+          const uint4 h = *reinterpret_cast<const uint4*>(cx.sbuf + off);
+          const uint4 l = *reinterpret_cast<const uint4*>(cx.sbuf + 4096 + off);
+          const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+          for (int e2 = 0; e2 < 4; ++e2) {
+            const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&hw[e2]));
+            const float2 lf = __half22float2(*reinterpret_cast<const __half2*>(&lw[e2]));
+            const int i = 8 * c8 + 2 * e2;
+            x[i] = fmaf(x[i], s2, -fmaf(hf.x, ss, lf.x * ss));
+            x[i + 1] = fmaf(x[i + 1], s2, -fmaf(hf.y, ss, lf.y * ss));
+          }
+        }
+        const int di = r - c0;
+        if (static_cast<unsigned>(di) < static_cast<unsigned>(W)) {
+#pragma unroll
+          for (int i = 0; i < W; ++i)
+            if (i == di) x[i] += cx.gam;
+        }
+#pragma unroll
+        for (int i = 0; i < W; ++i) cx.amax = nonneg_max(cx.amax, fabsf(x[i]));
+        if (jb.c_hi && split_now) put_split<W>(cx, jb.c_hi, jb.c_plane, jb.c_ld, c0, x, cx.inv_out, cx.ovf);
+        break;
+      }
       __half svh[W], svl[W];
       if (cx.sbuf) {  // W consecutive columns = W / 8 swizzled 16-byte chunks of this lane's row
 #pragma unroll
@@ -371,12 +402,16 @@ __device__ __forceinline__ void stage_direct(uint8_t* buf, const float (&acc)[64
     uint32_t hw[4], lw[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      __half h0, l0, h1, l1;
-      split_scaled(f(acc[8 * ch + 2 * i], c0 + 8 * ch + 2 * i) * inv, h0, l0);
-      split_scaled(f(acc[8 * ch + 2 * i + 1], c0 + 8 * ch + 2 * i + 1) * inv, h1, l1);
-      ovf |= __hisinf(h0) | __hisinf(h1) | __hisnan(h0) | __hisnan(h1);
-      hw[i] = static_cast<uint32_t>(__half_as_ushort(h0)) | (static_cast<uint32_t>(__half_as_ushort(h1)) << 16);
-      lw[i] = static_cast<uint32_t>(__half_as_ushort(l0)) | (static_cast<uint32_t>(__half_as_ushort(l1)) << 16);
+      // paired round-to-nearest conversions (bitwise the scalar split): hi = rn(y), lo = rn(y - hi); the hi
+      // half overflows (inf) or is NaN exactly when !(|y| < 65520)
+      const float y0 = f(acc[8 * ch + 2 * i], c0 + 8 * ch + 2 * i) * inv;
+      const float y1 = f(acc[8 * ch + 2 * i + 1], c0 + 8 * ch + 2 * i + 1) * inv;
+      const __half2 h = __floats2half2_rn(y0, y1);
+      const float2 hf = __half22float2(h);
+      const __half2 l = __floats2half2_rn(y0 - hf.x, y1 - hf.y);
+      ovf |= !(fabsf(y0) < 65520.f) | !(fabsf(y1) < 65520.f);
+      hw[i] = *reinterpret_cast<const uint32_t*>(&h);
+      lw[i] = *reinterpret_cast<const uint32_t*>(&l);
     }
     const int off = lane * 128 + ((ch ^ (lane & 7)) << 4);
     *reinterpret_cast<uint4*>(buf + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
@@ -478,7 +513,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
   const int nacc = ring ? static_cast<int>(kSl) : nacc_req;  // accumulators per tile (1, 2 or 4; 1 for NT = 256)
   const bool mc = PASSES == 3 && nacc == 2;  // main (hi*hi) + correction (hi*lo + lo*hi) accumulators
   const bool mc4 = PASSES == 3 && nacc == 4 && !ring;  // three K-range main accumulators + correction
-  const int xp = nacc_in >> 8;  // DASH_EXP knobs: timing 1 hi planes only, 2 no epilogue, 4 no staging, 8 no bulk stores, 16 L2 prefetch; 32 mirror via global stores (valid, 2-3% slower); 64 / 128 plain (unhinted) split stores / operand loads
+  const int xp = nacc_in >> 8;  // DASH_EXP knobs: timing 1 hi planes only, 2 no epilogue, 4 no staging, 8 no bulk stores, 16 L2 prefetch; 32 mirror via global stores (valid, 2-3% slower); 64 / 128 plain (unhinted) split stores / operand loads; 256 no side-input load
   const uint32_t nsets = kSl / nacc;         // tiles in flight in TMEM
 
   if (gate && *gate == 0) return;  // uniform across the grid (and thus across each pair)
@@ -823,7 +858,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         const bool f_tma = jb.f_map >= 0;
         const bool fin_tma = f_tma && jb.op == EPI_EMA;
         __syncwarp();                 // every lane is done with the previous tile's staging buffer
-        if ((side_tma || fin_tma) && lane == 0) {  // stage the side / fp32 input tile while the MMAs run
+        const bool side_load = side_tma && !(xp & 256);  // (knob 256: timing without the side-input load)
+        if ((side_load || fin_tma) && lane == 0) {  // stage the side / fp32 input tile while the MMAs run
           wait_reads();          // the previous tile's bulk stores have read the buffer
           mbar_arrive_expect_tx(&sbar[warp - 2], 8192);
           const int tc0 = n0 + 64 * hc, tr0 = m0 + kHalf * static_cast<int>(rank) + 32 * q;
@@ -931,8 +967,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         cx.lane = static_cast<int>(lane);
         cx.lc0 = n0 + 64 * hc;
         if (side_tma || fin_tma) {
-          mbar_wait(&sbar[warp - 2], sphase);
-          sphase ^= 1u;
+          if (side_load || fin_tma) {
+            mbar_wait(&sbar[warp - 2], sphase);
+            sphase ^= 1u;
+          }
           if (side_tma) cx.sbuf = ebuf;
           else cx.fbuf = ebuf;
         }

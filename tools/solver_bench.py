@@ -1,6 +1,6 @@
 """GEMM / solver micro-benchmark on one B200 (development tool, not part of the product path).
 
-    python tools/solver_bench.py --n 256 --b 1024 --iters 10 [--mode f32|f16]
+    python tools/solver_bench.py --n 256 --b 1024 --iters 10 [--mode f32|f16] [--solver ndb|cheb]
 
 Times (CUDA events, per tcgen05 launch) a standalone batched product and a fixed-iteration Newton-DB
 solve on a seeded SPD stack, and prints per-launch-kind ms and algorithmic TFLOP/s (2 B^3 per product).
@@ -50,6 +50,8 @@ def main() -> None:
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--mode", default="f32", choices=["f64", "f32", "f16"])
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--solver", default="ndb", choices=["ndb", "cheb"])
+    ap.add_argument("--degree", type=int, default=60)
     args = ap.parse_args()
     mode = {"f64": PrecisionMode.FULL64, "f32": PrecisionMode.EMULATED32, "f16": PrecisionMode.F16}[args.mode]
     a = spd_stack(args.n, args.b)
@@ -64,6 +66,25 @@ def main() -> None:
     torch.cuda.synchronize()
     report("bmm", _lib.gemm_timing_list())
     _lib.gemm_timing(False)
+    if args.solver == "cheb":
+        from paper_2602_02016_b200.chebyshev import clenshaw_split, fit_inverse_root
+
+        coef = fit_inverse_root(4, degree=args.degree, num_points=1000, interval=(1e-10, 1.0 + 1e-10))
+        one = torch.ones(args.n, device="cuda")
+        out = SplitStack(args.n, args.b, args.b)
+        clenshaw_split(sa, coef, one, one, None, out, mode)
+        torch.cuda.synchronize()
+        _lib.gemm_timing(True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.reps):
+            clenshaw_split(sa, coef, one, one, None, out, mode)
+        e1.record()
+        torch.cuda.synchronize()
+        report("cheb", _lib.gemm_timing_list())
+        _lib.gemm_timing(False)
+        print(f"  cheb wall (events) {e0.elapsed_time(e1) / args.reps:.2f} ms per evaluation")
+        return
     ndb_split(sa, None, 0.0, args.iters, mode)
     torch.cuda.synchronize()
     _lib.gemm_timing(True)
