@@ -99,10 +99,12 @@ int dash_ndb(const dash_stack* a, const float* inv_scale, const dash_stack* y, c
  *   the block diagonal are valid, diagonal blocks complete) -- the optimizer completes only the
  *   output it reads; the input a may itself be upper-stored (dash_ndb accepts that too).  dash_fill_lower
  *   completes such a stack in place (lower blocks <- transposed upper);
- *   both are plain dash_ndb / a no-op when the iterates are stored complete (DASH_NDB_UP=0, DASH_KB=32). */
+ *   both are plain dash_ndb / a no-op when the iterates are stored complete (DASH_NDB_UP=0, DASH_KB=32).
+ *   outputs: the outputs the caller reads (1 = y, 2 = z, 3 = both); the last iteration computes only those
+ *   (the other stack then holds an earlier iterate). */
 int dash_ndb_upper(const dash_stack* a, const float* inv_scale, const dash_stack* y, const dash_stack* z, float tol,
-                   float stall, int max_iters, int passes, int* iters, float* resid, int* conv, void* ws, size_t ws_bytes,
-                   void* stream);
+                   float stall, int max_iters, int passes, int outputs, int* iters, float* resid, int* conv, void* ws,
+                   size_t ws_bytes, void* stream);
 int dash_fill_lower(const dash_stack* s, void* stream);
 size_t dash_cn_ws_bytes(int n, int b);
 int dash_cn(const dash_stack* a, const float* inv_scale, int p, float c, const dash_stack* x, float tol,

@@ -60,8 +60,8 @@ _SIGNATURES: dict[str, tuple] = {
     "dash_ndb_ws_bytes": (c_size_t, [c_int, c_int]),
     "dash_ndb": (c_int, [_P, c_void_p, _P, _P, c_float, c_float, c_int, c_int, c_void_p, c_void_p, c_void_p,
                          c_void_p, c_size_t, c_void_p]),
-    "dash_ndb_upper": (c_int, [_P, c_void_p, _P, _P, c_float, c_float, c_int, c_int, c_void_p, c_void_p, c_void_p,
-                               c_void_p, c_size_t, c_void_p]),
+    "dash_ndb_upper": (c_int, [_P, c_void_p, _P, _P, c_float, c_float, c_int, c_int, c_int, c_void_p, c_void_p,
+                               c_void_p, c_void_p, c_size_t, c_void_p]),
     "dash_fill_lower": (c_int, [_P, c_void_p]),
     "dash_cn_ws_bytes": (c_size_t, [c_int, c_int]),
     "dash_cn": (c_int, [_P, c_void_p, c_int, c_float, _P, c_float, c_float, c_int, c_int, c_void_p, c_void_p,

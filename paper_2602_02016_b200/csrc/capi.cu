@@ -25,14 +25,14 @@ int dash_ndb(const dash_stack* a, const float* inv_scale, const dash_stack* y, c
 }
 
 int dash_ndb_upper(const dash_stack* a, const float* inv_scale, const dash_stack* y, const dash_stack* z, float tol,
-                   float stall, int max_iters, int passes, int* iters, float* resid, int* conv, void* ws, size_t ws_bytes,
-                   void* stream) {
+                   float stall, int max_iters, int passes, int outputs, int* iters, float* resid, int* conv, void* ws,
+                   size_t ws_bytes, void* stream) {
   if (!square_same(a, y) || !square_same(a, z) || max_iters < 1 || tol < 0.f || stall < 0.f || !iters || !resid || !conv ||
-      (passes != 1 && passes != 3 && passes != 4))
+      (passes != 1 && passes != 3 && passes != 4) || outputs < 1 || outputs > 3)
     return DASH_EINVAL;
   if (ws_bytes < ndb_ws_bytes(a->nmat, a->rows)) return DASH_EINVAL;
   return ndb_solve(*a, inv_scale, *y, *z, tol, stall, max_iters, passes, iters, resid, conv, ws, ws_bytes,
-                   static_cast<cudaStream_t>(stream), nullptr, false);
+                   static_cast<cudaStream_t>(stream), nullptr, false, outputs);
 }
 
 int dash_fill_lower(const dash_stack* s, void* stream) {

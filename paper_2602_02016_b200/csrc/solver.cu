@@ -517,13 +517,16 @@ int fill_lower(const dash_stack& s, cudaStream_t st) {
 // ---------------------------------------------------------------------------- NDB
 size_t ndb_ws_bytes(int n, int b) {  // NOLINT
   const size_t stacks = 3 * stack_bytes(n, b, b);
-  const size_t jobs = 4 * JobBuilder::bytes_for(32, 2 * n) + JobBuilder::bytes_for(32, n);
+  const size_t jobs = 4 * JobBuilder::bytes_for(32, 2 * n) + 3 * JobBuilder::bytes_for(32, n);
   return stacks + jobs + state_bytes(n) + 4096;
 }
 
+// need: the outputs the caller reads (1 = y, 2 = z, 3 = both).  The last iteration computes only those (the
+// optimizer reads Y of the first p = 4 chain and Z otherwise, shampoo.py:332-340): one product fewer per chain.
 int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_out, const dash_stack& z_out,
               float tol, float stall, int max_iters, int passes, int* iters, float* resid_out, int* conv, void* ws,
-              size_t ws_bytes, cudaStream_t st, int* products, bool complete) {
+              size_t ws_bytes, cudaStream_t st, int* products, bool complete, int need) {
+  if (need < 1 || need > 3) return DASH_EINVAL;
   const int n = a.nmat;
   Arena ar(ws, ws_bytes);
   dash_stack e, y2, z2;
@@ -534,7 +537,7 @@ int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_o
   // ping-pong: (Y, Z) at even iterations live in (y_out, z_out), odd ones in (y2, z2)
   const dash_stack ys[2] = {y_out, y2};
   const dash_stack zs[2] = {z_out, z2};
-  UploadedGemm g_first, g_e[2], g_yz[2];
+  UploadedGemm g_first, g_e[2], g_yz[2], g_last[2];
   const int up = ndb_upper_storage() ? 1 : 0;
   {
     JobBuilder jb;  // Y1 = (a E1) * inv_scale
@@ -589,6 +592,21 @@ int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_o
       jy.push(j);
     }
     if (!jy.upload(ar, st, &g_yz[par])) return DASH_EINVAL;
+    if (need != 3) {  // the last iteration: the read output only
+      JobBuilder jl;
+      for (int m = 0; m < n; ++m) {
+        GemmJob j;
+        if (need == 1 ? !jl.operands(j, yc, m, 0, e, m, kSymB) : !jl.operands(j, e, m, 0, zc, m, kSymB))
+          return DASH_EINVAL;
+        j.op = EPI_SPLIT;
+        j.out_mat = m;
+        j.sym = 1;
+        j.a_up = j.b_up = j.c_up = up;
+        jl.set_out(j, need == 1 ? yn : zn, m);
+        jl.push(j);
+      }
+      if (!jl.upload(ar, st, &g_last[par])) return DASH_EINVAL;
+    }
   }
   int np = 0;
   state_init_kernel<<<(n + 255) / 256, 256, 0, st>>>(s, n);
@@ -611,8 +629,9 @@ int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_o
   note_launch();
   for (int k = 2; k <= max_iters; ++k) {
     if (int rc = g_e[par].run(passes, st, s.n_active)) return rc;
-    if (int rc = g_yz[par].run(passes, st, s.n_active)) return rc;
-    np += 3;
+    const bool last_only = k == max_iters && need != 3;
+    if (int rc = (last_only ? g_last[par] : g_yz[par]).run(passes, st, s.n_active)) return rc;
+    np += last_only ? 2 : 3;
     const bool more = k < max_iters;  // the next iteration writes (Y, Z)[par] (par flips below)
     freeze_kernel<<<1, 1024, 0, st>>>(s, n, k, tol, stall, 0, iters, resid_out, conv, nullptr,
                                       more ? e.amax : nullptr, more ? ys[par].amax : nullptr,
@@ -622,11 +641,11 @@ int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_o
   }
   finish_kernel<<<(n + 255) / 256, 256, 0, st>>>(s, n, max_iters, iters, resid_out, conv);
   note_launch();
-  copy_stack_if(s.par, 1, y_out, y2, st);  // final iterate in the scratch pair -> outputs
-  copy_stack_if(s.par, 1, z_out, z2, st);
+  if (need & 1) copy_stack_if(s.par, 1, y_out, y2, st);  // final iterate in the scratch pair -> outputs
+  if (need & 2) copy_stack_if(s.par, 1, z_out, z2, st);
   if (up && complete) {  // (complete = false: the caller completes only the outputs it reads)
-    fill_lower(y_out, st);
-    fill_lower(z_out, st);
+    if (need & 1) fill_lower(y_out, st);
+    if (need & 2) fill_lower(z_out, st);
   }
   if (products) *products = np;
   return cuda_ok();

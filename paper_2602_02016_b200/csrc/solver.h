@@ -11,7 +11,7 @@ bool ndb_upper_storage();   // the NDB iterates use upper pair-block storage (ty
 int fill_lower(const dash_stack& s, cudaStream_t st);  // lower pair blocks <- transposed upper ones
 int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_out, const dash_stack& z_out,
               float tol, float stall, int max_iters, int passes, int* iters, float* resid_out, int* conv, void* ws,
-              size_t ws_bytes, cudaStream_t st, int* products, bool complete = true);
+              size_t ws_bytes, cudaStream_t st, int* products, bool complete = true, int need = 3);
 size_t cn_ws_bytes(int n, int b);
 int cn_solve(const dash_stack& a, const float* inv_scale, int p, float c, const dash_stack& x_out, float tol,
              float stall, int max_iters, int passes, int* iters, float* resid_out, int* conv, void* ws, size_t ws_bytes,

@@ -98,12 +98,15 @@ def _reports(n: int, dev, scratch: Scratch | None, tag: str) -> DeviceReports:
 
 def ndb_split(a: SplitStack, inv_scale: torch.Tensor | None, tol: float, max_iters: int,
               mode: PrecisionMode, complete: bool = True, *, stall: float | None = None,
-              scratch: Scratch | None = None, tag: str = "ndb") -> tuple[SplitStack, SplitStack, DeviceReports]:
+              scratch: Scratch | None = None, tag: str = "ndb", outputs: str = "yz"
+              ) -> tuple[SplitStack, SplitStack, DeviceReports]:
     """NDB on split stacks (device-resident fast path used by the optimizer).
 
     ``complete=False`` leaves Y and Z in upper pair-block storage (``dash_ndb_upper``); complete the one you
-    read with :func:`fill_lower`.  ``stall``: the stall cap (default: ``linalg.stall_for(tol, mode)``).
-    ``scratch``: reuse the output / workspace buffers of a previous call with the same ``tag``."""
+    read with :func:`fill_lower`.  ``outputs`` ("y", "z" or "yz", with ``complete=False``): the iterates the
+    caller reads -- the last iteration computes only those, the other stack holds an earlier iterate.
+    ``stall``: the stall cap (default: ``linalg.stall_for(tol, mode)``).  ``scratch``: reuse the output /
+    workspace buffers of a previous call with the same ``tag``."""
     n, b = a.nmat, a.rows
     dev = a.data.device
     if scratch is not None:
@@ -114,9 +117,14 @@ def ndb_split(a: SplitStack, inv_scale: torch.Tensor | None, tol: float, max_ite
     L = _lib.lib()
     nbytes = L.dash_ndb_ws_bytes(n, b)
     ws = scratch.ws("solver", nbytes) if scratch is not None else workspace(nbytes, dev)
+    need = {"y": 1, "z": 2, "yz": 3}[outputs]
+    if complete and need != 3:
+        raise ValueError("outputs selects iterates of the upper-stored solve (complete=False) only")
+    args = [float(tol), float(stall_for(tol, mode) if stall is None else stall), int(max_iters), passes_for(mode)]
+    if not complete:
+        args.append(need)
     fn = L.dash_ndb if complete else L.dash_ndb_upper
-    st = fn(a.ref(), inv_scale.data_ptr() if inv_scale is not None else None, y.ref(), z.ref(),
-            float(tol), float(stall_for(tol, mode) if stall is None else stall), int(max_iters), passes_for(mode),
+    st = fn(a.ref(), inv_scale.data_ptr() if inv_scale is not None else None, y.ref(), z.ref(), *args,
             rep.iters.data_ptr(), rep.resid.data_ptr(), rep.conv.data_ptr(), ws.data_ptr(), ws.numel(),
             _lib.stream_ptr())
     _lib.check(st, "dash_ndb")

@@ -688,13 +688,13 @@ def _refresh_range(state: ShampooState, cfg: ShampooConfig, gi: int, s: int, e: 
         # the iterates stay in upper pair-block storage (the second solve of a 4th root reads Y1 that way); only
         # the root that is read next is completed
         _, src, rep = ndb_split(a, inv, solver.tolerance, solver.max_iters, mode, complete=False, scratch=sc,
-                                tag="ndb1")
+                                tag="ndb1", outputs="z")
         reps = [rep]
-    else:
+    else:  # (each chain's last iteration computes only the iterate read next: Y1, then Z2)
         y1, _, r1 = ndb_split(a, inv, solver.tolerance, solver.max_iters, mode, complete=False, scratch=sc,
-                              tag="ndb1")
+                              tag="ndb1", outputs="y")
         _, src, r2 = ndb_split(y1, None, solver.tolerance, solver.max_iters, mode, complete=False, scratch=sc,
-                               tag="ndb2")
+                               tag="ndb2", outputs="z")
         reps = [r1, r2]
     fallback = None
     if tol_mode:  # per-block reports, in the reference's order (first chain, then second)

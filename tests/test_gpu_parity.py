@@ -241,6 +241,24 @@ def test_ndb_upper_storage_fill_matches_complete(b):
     assert float((zf - zf.transpose(1, 2)).abs().max()) < 1e-5 * float(zf.abs().max())
 
 
+@pytest.mark.parametrize("outputs", ["y", "z"])
+def test_ndb_selected_output_bitwise(outputs):
+    """dash_ndb_upper computing only the read iterate in its last iteration: that iterate is bit-identical to the
+    two-output solve's (fixed iterations and tolerance mode with early-converged blocks)."""
+    import torch
+
+    from paper_2602_02016_b200.linalg import PrecisionMode, SplitStack
+
+    a = np.stack([core.random_spd(512, c, seed=50 + i, scale=0.5) for i, c in enumerate([10.0, 1e2, 1.5])])
+    sa = SplitStack.from_float(torch.tensor(a, dtype=torch.float32, device="cuda"))
+    for tol, iters in ((0.0, 7), (1e-4, 12)):
+        y, z, r = roots.ndb_split(sa, None, tol, iters, PrecisionMode.EMULATED32, complete=False)
+        ys, zs, rs = roots.ndb_split(sa, None, tol, iters, PrecisionMode.EMULATED32, complete=False, outputs=outputs)
+        want, got = (y, ys) if outputs == "y" else (z, zs)
+        assert torch.equal(roots.fill_lower(want).to_float(), roots.fill_lower(got).to_float())
+        assert torch.equal(r.iters, rs.iters) and torch.equal(r.resid, rs.resid)
+
+
 def test_ndb_chain_reads_upper_stored_input():
     """Inverse 4th root chain: the second solve on the upper-stored Y1 == on the completed Y1 (bitwise)."""
     import torch
