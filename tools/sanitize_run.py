@@ -33,6 +33,11 @@ def main() -> None:
         sa = SplitStack.from_float(st)
         _, z, _ = roots.ndb_split(sa, None, 0.0, 3, mode, complete=False)
         roots.fill_lower(z)
+        y, _, _ = roots.ndb_split(sa, None, 0.0, 3, mode, complete=False, outputs="y")  # last iteration: Y only
+        roots.fill_lower(y)
+        c2 = chebyshev.fit_inverse_root(4, degree=6)  # Clenshaw on the split stack (fused full-piece epilogue)
+        ones = torch.ones(2, device="cuda")
+        chebyshev.clenshaw_split(sa, c2, ones, ones, None, SplitStack(2, 256, 256), mode)
         roots.batched_coupled_newton(st, roots.CnConfig(p=4, tolerance=0.0, max_iters=2), mode)
     chebyshev.batched_clenshaw_matrix(st, chebyshev.fit_inverse_root(4, degree=6), np.ones(2))
     n = 3
