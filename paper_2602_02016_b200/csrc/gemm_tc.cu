@@ -978,7 +978,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         for (int j = 0; j < 4; ++j) {
           const int c0 = n0 + 64 * hc + 16 * j;
           float (&v)[16] = *reinterpret_cast<float(*)[16]>(&acc[16 * j]);  // in place: final values stay in acc
-          if (c0 < jb.N && !(xp & 2)) epi_piece<16>(jb, cx, c0, v, !tma_out);
+          // (a symmetric job's sub-block below the diagonal is neither stored nor reduced: skip its math)
+          if (c0 < jb.N && cx.store && !(xp & 2)) epi_piece<16>(jb, cx, c0, v, !tma_out);
         }
         if ((tma_out || f_tma) && cx.store && !(xp & 2)) {
           // ---- staged bulk-tensor stores of the split output(s), direct and (symmetric jobs) mirrored
