@@ -695,19 +695,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         // `nmain` slots by K range: nacc == 2 -> one main slot over the whole K; nacc == 4 -> three main slots of
         // K / 3 each (shorter truncating accumulation chains, FULL64).  Unsplit products (fp16, or DASH_NACC=1)
         // put every pass into slot c = K range c of nacc.
-        if (ring) {  // ---- ring mode: units of per_u k-blocks, unit u -> slot u % kSl
-          const int per_u = (nk + nring - 1) / nring;
+        if (ring) {  // ---- ring mode: units of per_u 16-wide k steps, unit u -> slot u % kSl
+          const int per_u = (nk * (KB / 16) + nring - 1) / nring;
           uint32_t u = ucount;  // the current unit (counters, not divisions: this loop is issue-latency bound)
-          int kin = 0;          // k-blocks of the current unit issued
+          int kin = 0;          // k steps of the current unit issued
           for (int kb = 0; kb < nk; ++kb) {
-            const bool first = kin == 0;
-            const uint32_t slot = u % kSl;
-            if (first) {
-              const long long w0 = prof ? clock64() : 0;
-              mbar_wait(&tempty[slot], ((u / kSl) & 1u) ^ 1u);
-              if (prof) pw0 += clock64() - w0;
-              tc_fence_after();
-            }
             const int a_mn = jb.a_mn ^ static_cast<int>(a_up && upper_flip(jb.a_mn, ti, (kb * KB) >> 8));
             const int b_mn = jb.b_mn ^ static_cast<int>(b_up && upper_flip(jb.b_mn, bpb, (kb * KB) >> 8));
             const uint32_t idesc = umma_idesc_f16(kPairM, kPN, a_mn, b_mn);
@@ -725,21 +717,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             const uint32_t b_base = a_base + C::kABytes * C::kPlanes;
 #pragma unroll
             for (int k = 0; k < KB / 16; ++k) {
+              const uint32_t slot = u % kSl;
+              if (kin == 0) {
+                const long long w0 = prof ? clock64() : 0;
+                mbar_wait(&tempty[slot], ((u / kSl) & 1u) ^ 1u);
+                if (prof) pw0 += clock64() - w0;
+                tc_fence_after();
+              }
 #pragma unroll
               for (int p = 0; p < PASSES; ++p) {
                 const uint32_t ap = (p == 2) ? 1u : 0u, bp = (p == 1) ? 1u : 0u;
                 const uint64_t ad = umma_sdesc(a_base + ap * C::kABytes + k * a_kstep, a_lbo, a_sbo, a_lay);
                 const uint64_t bd = umma_sdesc(b_base + bp * C::kBBytes + k * b_kstep, b_lbo, b_sbo, b_lay);
-                umma2_f16_elect(tmem_base + slot * kPN, ad, bd, idesc, (first && k == 0 && p == 0) ? 0u : 1u);
+                umma2_f16_elect(tmem_base + slot * kPN, ad, bd, idesc, (kin == 0 && p == 0) ? 0u : 1u);
+              }
+              if (++kin == per_u || (kb == nk - 1 && k == KB / 16 - 1)) {
+                umma2_commit_mc_elect(&tfull[slot]);
+                ++u;
+                kin = 0;
               }
             }
             umma2_commit_mc_elect(&empty[stage]);
             if (++stage == C::kStages) { stage = 0; phase ^= 1; }
-            if (++kin == per_u || kb == nk - 1) {
-              umma2_commit_mc_elect(&tfull[slot]);
-              ++u;
-              kin = 0;
-            }
           }
           ucount = u;
           continue;
@@ -872,7 +871,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         }
         float acc[64];
         // ring mode: drain the tile's units in issue order (unit u -> slot u % kSl), summing in registers
-        const int nunits = ring ? (nk + (nk + nring - 1) / nring - 1) / ((nk + nring - 1) / nring) : nacc;
+        const int nsteps = nk * (KB / 16), per_us = ring ? (nsteps + nring - 1) / nring : 1;
+        const int nunits = ring ? (nsteps + per_us - 1) / per_us : nacc;
         for (int c = 0; c < nunits; ++c) {
           if (ring) {
             const uint32_t u = ucount + static_cast<uint32_t>(c), slot = u % kSl;
@@ -1175,9 +1175,11 @@ int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtenso
   // tensor-core accumulation chain covers K / 16; B = 1024 Newton-DB error ~14x smaller than the main +
   // correction default, ~20% slower); otherwise the DASH_NACC default
   int nacc_req = 0;
-  if (passes == 4) {
+  int kb_force = 0;
+  if (passes == 4) {  // FULL64: 32-wide K blocks and one ring unit per K block (32-long truncating chains)
     passes = 3;
-    nacc_req = 16;
+    nacc_req = 32;
+    kb_force = 32;
     issued *= 0.75;
   }
   const int wm = wide_mode();
@@ -1235,13 +1237,14 @@ int gemm_launch(const GemmJob* d_jobs, int njobs, int total_tiles, const CUtenso
     if (g_kb != 32 && g_kb != 64) g_kb = kKbDefault;
   }
   const int flags = (passes == 3 ? (nacc_req ? nacc_req : g_nacc) : 1) | (g_exp << 8);
-  if (use_wide && passes == 3 && g_kb == 64) launch_variant<3, 64, 256>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter, prof);
+  const int kb = kb_force ? kb_force : g_kb;
+  if (use_wide && passes == 3 && kb == 64) launch_variant<3, 64, 256>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter, prof);
   else if (use_wide && passes == 3) launch_variant<3, 32, 256>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter, prof);
-  else if (use_wide && g_kb == 64) launch_variant<1, 64, 256>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter, prof);
+  else if (use_wide && kb == 64) launch_variant<1, 64, 256>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter, prof);
   else if (use_wide) launch_variant<1, 32, 256>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter, prof);
-  else if (passes == 3 && g_kb == 64) launch_variant<3, 64>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter, prof);
+  else if (passes == 3 && kb == 64) launch_variant<3, 64>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter, prof);
   else if (passes == 3) launch_variant<3, 32>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter, prof);
-  else if (g_kb == 64) launch_variant<1, 64>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter, prof);
+  else if (kb == 64) launch_variant<1, 64>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter, prof);
   else launch_variant<1, 32>(grid2, stream, d_jobs, njobs, total_tiles, d_maps, gate, flags, uniform, counter, prof);
   if (e1) cudaEventRecord(e1, stream);
   if (prof) {  // diagnostics: per-launch wait-cycle breakdown (serialises the stream)

@@ -487,6 +487,8 @@ bool ndb_upper_storage() {
   static const int on = getenv("DASH_NDB_UP") ? atoi(getenv("DASH_NDB_UP")) : 1;
   return on && gemm_kblock() == 64;
 }
+// passes = 4 (FULL64) launches run the K-block 32 kernel (gemm_launch), which reads operands complete
+bool ndb_upper_storage(int passes) { return passes != 4 && ndb_upper_storage(); }
 
 // Lower pair blocks of an upper-stored split stack <- transposes of the upper ones (both planes), through
 // 32x32 shared-memory tiles (coalesced reads and writes).
@@ -538,7 +540,7 @@ int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_o
   const dash_stack ys[2] = {y_out, y2};
   const dash_stack zs[2] = {z_out, z2};
   UploadedGemm g_first, g_e[2], g_yz[2], g_last[2];
-  const int up = ndb_upper_storage() ? 1 : 0;
+  const int up = ndb_upper_storage(passes) ? 1 : 0;
   {
     JobBuilder jb;  // Y1 = (a E1) * inv_scale
     for (int m = 0; m < n; ++m) {
@@ -678,7 +680,7 @@ int cn_solve(const dash_stack& a, const float* inv_scale, int p, float c, const 
   if (!ar.ok) return DASH_EINVAL;
   const dash_stack xs[2] = {x_out, x2};
   const dash_stack ms[2] = {m1, m2};
-  const int up = ndb_upper_storage() ? 1 : 0;  // X, M, C are polynomials in a: upper pair-block storage
+  const int up = ndb_upper_storage(passes) ? 1 : 0;  // X, M, C are polynomials in a: upper pair-block storage
   UploadedGemm g_xc[2], g_c4, g_m[2];
   for (int par = 0; par < 2; ++par) {
     JobBuilder j1;  // X' = X C and C2 = C C in one launch
@@ -841,7 +843,7 @@ int cheb_solve(const dash_stack& a, const float* inv_scale, const float* mult, c
   // rotation r holds the jobs for every k with k % 3 == r: B_k = 2 S B_{k+1} - B_{k+2} + c_k I.  The B_k are
   // polynomials in S, stored as upper pair blocks (the side input is read only at stored positions); the
   // final product reads B_1 that way and writes complete outputs.
-  const int up = ndb_upper_storage() ? 1 : 0;
+  const int up = ndb_upper_storage(passes) ? 1 : 0;
   UploadedGemm g_rot[3], g_fin;
   for (int r = 0; r < 3; ++r) {
     JobBuilder jb;

@@ -7,7 +7,8 @@
 namespace dash {
 
 size_t ndb_ws_bytes(int n, int b);
-bool ndb_upper_storage();   // the NDB iterates use upper pair-block storage (types.h)
+bool ndb_upper_storage();
+bool ndb_upper_storage(int passes);  // false for passes = 4 (FULL64 runs the K-block 32 kernel)   // the NDB iterates use upper pair-block storage (types.h)
 int fill_lower(const dash_stack& s, cudaStream_t st);  // lower pair blocks <- transposed upper ones
 int ndb_solve(const dash_stack& a, const float* inv_scale, const dash_stack& y_out, const dash_stack& z_out,
               float tol, float stall, int max_iters, int passes, int* iters, float* resid_out, int* conv, void* ws,

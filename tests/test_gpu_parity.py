@@ -188,10 +188,11 @@ def test_c1_config_fixed_iterations_vs_oracle():
     ost = core.init_state([w], ocfg)
     oout, ost, _ = core.step(ost, [w], [g], ocfg, seed=0)
     # literal C1 blocks have cond ~1e6 after one EMA step; FULL64 (the default precision) runs
-    # the statistics, solver and apply products in 16 K ranges per tile
+    # the statistics, solver and apply products on 32-wide K blocks with every 16-wide k step (B <= 512) in its own
+    # TMEM accumulation unit: measured 9.5e-4, the true-fp32 level SURVEY §7.3.3 quotes (1e-4 - 1e-3)
     err = relf(out[0] - w, oout[0] - w)
     print(f"C1 fixed-10 update relF {err:.2e}")
-    assert err < 5e-3
+    assert err < 1.5e-3
     # the update norm identity holds per block regardless of conditioning
     assert np.linalg.norm(out[0] - w) == pytest.approx(np.linalg.norm(oout[0] - w), rel=1e-4)
 
