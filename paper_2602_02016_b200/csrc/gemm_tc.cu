@@ -695,9 +695,59 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         // `nmain` slots by K range: nacc == 2 -> one main slot over the whole K; nacc == 4 -> three main slots of
         // K / 3 each (shorter truncating accumulation chains, FULL64).  Unsplit products (fp16, or DASH_NACC=1)
         // put every pass into slot c = K range c of nacc.
-        if (ring) {  // ---- ring mode: units of per_u 16-wide k steps, unit u -> slot u % kSl
-          const int per_u = (nk * (KB / 16) + nring - 1) / nring;
+        const int per_us = ring ? (nk * (KB / 16) + nring - 1) / nring : 0;  // k steps per ring unit
+        if (ring && per_us % (KB / 16) == 0) {  // ---- ring mode, units of whole k blocks (the usual case)
+          const int per_u = per_us / (KB / 16);
           uint32_t u = ucount;  // the current unit (counters, not divisions: this loop is issue-latency bound)
+          int kin = 0;          // k-blocks of the current unit issued
+          for (int kb = 0; kb < nk; ++kb) {
+            const bool first = kin == 0;
+            const uint32_t slot = u % kSl;
+            if (first) {
+              const long long w0 = prof ? clock64() : 0;
+              mbar_wait(&tempty[slot], ((u / kSl) & 1u) ^ 1u);
+              if (prof) pw0 += clock64() - w0;
+              tc_fence_after();
+            }
+            const int a_mn = jb.a_mn ^ static_cast<int>(a_up && upper_flip(jb.a_mn, ti, (kb * KB) >> 8));
+            const int b_mn = jb.b_mn ^ static_cast<int>(b_up && upper_flip(jb.b_mn, bpb, (kb * KB) >> 8));
+            const uint32_t idesc = umma_idesc_f16(kPairM, kPN, a_mn, b_mn);
+            const uint32_t a_lbo = a_mn ? KB * 128u : 16u, b_lbo = b_mn ? KB * 128u : 16u;
+            const uint32_t a_kstep = a_mn ? 2048u : 32u, b_kstep = b_mn ? 2048u : 32u;
+            const uint32_t a_sbo = a_mn ? 1024u : (KB == 64 ? 1024u : 512u), b_sbo = b_mn ? 1024u : (KB == 64 ? 1024u : 512u);
+            const uint32_t a_lay = a_mn ? 2u : (KB == 64 ? 2u : 4u), b_lay = b_mn ? 2u : (KB == 64 ? 2u : 4u);
+            {
+              const long long w0 = prof ? clock64() : 0;
+              mbar_wait(&full[stage], phase);
+              if (prof) pw1 += clock64() - w0;
+            }
+            tc_fence_after();
+            const uint32_t a_base = smem_u32(smem + stage * C::kStageBytes);
+            const uint32_t b_base = a_base + C::kABytes * C::kPlanes;
+#pragma unroll
+            for (int k = 0; k < KB / 16; ++k) {
+#pragma unroll
+              for (int p = 0; p < PASSES; ++p) {
+                const uint32_t ap = (p == 2) ? 1u : 0u, bp = (p == 1) ? 1u : 0u;
+                const uint64_t ad = umma_sdesc(a_base + ap * C::kABytes + k * a_kstep, a_lbo, a_sbo, a_lay);
+                const uint64_t bd = umma_sdesc(b_base + bp * C::kBBytes + k * b_kstep, b_lbo, b_sbo, b_lay);
+                umma2_f16_elect(tmem_base + slot * kPN, ad, bd, idesc, (first && k == 0 && p == 0) ? 0u : 1u);
+              }
+            }
+            umma2_commit_mc_elect(&empty[stage]);
+            if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+            if (++kin == per_u || kb == nk - 1) {
+              umma2_commit_mc_elect(&tfull[slot]);
+              ++u;
+              kin = 0;
+            }
+          }
+          ucount = u;
+          continue;
+        }
+        if (ring) {  // ---- ring mode, units of per_u 16-wide k steps (shorter than a k block: FULL64, B <= 512)
+          const int per_u = per_us;
+          uint32_t u = ucount;
           int kin = 0;          // k steps of the current unit issued
           for (int kb = 0; kb < nk; ++kb) {
             const int a_mn = jb.a_mn ^ static_cast<int>(a_up && upper_flip(jb.a_mn, ti, (kb * KB) >> 8));
