@@ -383,7 +383,7 @@ def run_dash(args):
     per_launch = _lib.gemm_timing_list()
     _lib.gemm_timing(False)
     gemm_issued = sum(x[2] for x in per_launch)
-    launches = (_lib.launch_count() - launches0) // args.steps
+    launches = _lib.launch_count() - launches0  # every library kernel launched in the timed region (K steps)
     ms = ms_local
     if world > 1:
         t = torch.tensor([ms_local], device="cuda")
@@ -507,7 +507,7 @@ def run_dash(args):
             "gemm_launches_timed": n_gemm,
             "gemm_ms_per_step": round(gemm_ms / args.steps, 3),
         },
-        "gpu_launches": int(launches),
+        "gpu_launches": int(launches), "gpu_launches_per_step": int(launches) // args.steps,
         "clocks": clk.summary(),
         "e2e": e2e,
     }
@@ -615,7 +615,7 @@ def run_train(args):
         ev1.record()
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.steps
-    launches = (_lib.launch_count() - launches0) // args.steps
+    launches = _lib.launch_count() - launches0  # every library kernel launched in the timed region (K steps)
     fwd_bwd = statistics.mean(a.elapsed_time(b) for a, b in zip([ev0] + events["applied"][:-1], events["backward_done"]))
     opt = statistics.mean(a.elapsed_time(b) for a, b in zip(events["backward_done"], events["applied"]))
     # end to end: the caller's token batch from pinned host memory, the loss read back every step
@@ -637,6 +637,7 @@ def run_train(args):
                    "seq_len": seq, "tokens_per_step": tokens, "parallelism": "single GPU"},
         "phases_ms": {"forward_backward": round(fwd_bwd, 3), "dash_step": round(opt, 3)},
         "tokens_per_s": round(tokens / (ms * 1e-3), 1), "final_loss": float(loss), "gpu_launches": int(launches),
+        "gpu_launches_per_step": int(launches) // args.steps,
         "clocks": clk.summary(),
         "e2e": {"value": round(e2e, 3), "unit": "ms", "h2d_bytes_per_step": tokens * 8 + batch * 8,
                 "d2h_bytes_per_step": 4},
